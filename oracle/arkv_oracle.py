@@ -309,7 +309,8 @@ def quantize(x: np.ndarray, bits: int, g: int, mode: str = "asym"):
             else:
                 s = F32(F32(mx - mn) / F32(2 ** bits - 1))
                 z = mn
-                c = np.array([np.rint(F32(F32(v - mn) / s)) for v in xs], dtype=np.int64)
+                # float32 array ops round each element exactly like the scalar ops
+                c = np.rint((xs - mn).astype(F32) / s).astype(np.int64)
                 c = np.clip(c, 0, 2 ** bits - 1)
         else:
             a = F32(np.abs(xs).max())
@@ -319,7 +320,7 @@ def quantize(x: np.ndarray, bits: int, g: int, mode: str = "asym"):
             else:
                 s = F32(a / F32(qmax))
                 z = F32(0.0)
-                c = np.array([np.rint(F32(v / s)) for v in xs], dtype=np.int64)
+                c = np.rint((xs / s).astype(F32)).astype(np.int64)
                 c = np.clip(c, -qmax, qmax)
         codes[gi * g:(gi + 1) * g] = c
         sc[gi] = s
@@ -417,12 +418,24 @@ class UnitCache:
         self.o_v = np.vstack([self.o_v, np.asarray(v, dtype=np.float64)[None]])
         self.n_pos = pos + 1
 
+    def ingest(self, k: np.ndarray, v: np.ndarray):
+        """The prompt's P tokens enter as Original at positions 0..P-1 (equivalent to
+        P appends on an empty unit)."""
+        if self.n_pos != 0:
+            raise ValueError("sequencing error (S:57)")
+        P = k.shape[0]
+        self.o_pos = np.arange(P, dtype=np.int64)
+        self.o_k = np.asarray(k, dtype=np.float64).copy()
+        self.o_v = np.asarray(v, dtype=np.float64).copy()
+        self.n_pos = P
+
     def keys_values(self):
         """Dequantized view of O ∪ Q (Alg. 1 'Reconstruction'), by state
         segment; the order does not affect attention (R26)."""
-        g, d = self.cfg.group_size, self.cfg.head_dim
-        qk = np.array([dequantize(self.q_kc[i], self.q_ks[i], self.q_kz[i], g) for i in range(self.n_q)]).reshape(self.n_q, d)
-        qv = np.array([dequantize(self.q_vc[i], self.q_vs[i], self.q_vz[i], g) for i in range(self.n_q)]).reshape(self.n_q, d)
+        g = self.cfg.group_size
+        # dequantize() applied to every Quantized row (vectorised over rows)
+        qk = self.q_kc * np.repeat(self.q_ks.astype(np.float64), g, axis=1) + np.repeat(self.q_kz.astype(np.float64), g, axis=1)
+        qv = self.q_vc * np.repeat(self.q_vs.astype(np.float64), g, axis=1) + np.repeat(self.q_vz.astype(np.float64), g, axis=1)
         pos = np.concatenate([self.o_pos, self.q_pos])
         return pos, np.vstack([self.o_k, qk]), np.vstack([self.o_v, qv])
 
@@ -554,8 +567,7 @@ class OracleARKV:
             for l in range(L):
                 for kvh in range(Hkv):
                     u = UnitCache(cfg)
-                    for p in range(P):
-                        u.append(p, k[b, l, kvh, p], v[b, l, kvh, p])
+                    u.ingest(k[b, l, kvh], v[b, l, kvh])
                     if prefill_needs_tailor(P, cfg):
                         if at is None:
                             at = {}

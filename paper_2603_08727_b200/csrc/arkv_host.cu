@@ -1,0 +1,703 @@
+// arkv_host.cu — host runtime behind the C ABI (include/arkv.h).
+//
+// Owns the data-independent count schedule (R9, R12, R14, R15): every (sequence,
+// layer) advances through counts the host knows without reading the device, so
+// the decode step never synchronizes.  Carves the caller's arena / workspace,
+// assigns arena slots (two-stack per unit plus staging slots for the tailor's
+// out-of-place compaction), and sequences the kernel launches.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <algorithm>
+#include <vector>
+
+#include "kernels.h"
+
+using namespace arkv;
+
+struct arkv_cache {
+  arkv_config cfg;
+  Geom g;
+  int device = 0;
+  // arena
+  uint8_t* slots = nullptr;
+  uint8_t* meta = nullptr;
+  UnitDesc* desc = nullptr;
+  int32_t* err = nullptr;
+  int n_slots = 0, n_spare = 0;
+  // workspace
+  float* partials = nullptr;
+  float* logits = nullptr;
+  int8_t* st_scratch = nullptr;
+  int32_t* src_scratch = nullptr;
+  float* pf_partials = nullptr;
+  float2* acc_pf = nullptr;
+  double* oq_tmp = nullptr;
+  double* colsum = nullptr;
+  int jobs_per_wave = 0, max_splits = 64, n_chunks1_max = 1;
+  // live kernel timing of the decode attention kernel (bench roofline)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;  // pairs
+  std::vector<double> ev_bytes;
+  int ev_used = 0;
+  bool fast = false;
+  // host mirrors
+  std::vector<double> rho;
+  std::vector<int> n_o, n_q, t_next, trig;  // per (b, l)
+  std::vector<int> unit_slot;               // per unit
+  std::vector<int> spare;
+  bool prefilled = false;
+  int64_t launches = 0;
+};
+
+namespace {
+
+constexpr int kPfChunkHost = 2048;
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct Sizes {
+  Geom g;
+  int n_spare, jobs_per_wave, max_splits, n_chunks1;
+  int64_t arena, ws;
+  int64_t off_meta, off_desc, off_err;
+  int64_t w_partials, w_logits, w_st, w_src, w_pfp, w_accpf, w_oq, w_colsum;
+};
+
+int64_t cost_o(const arkv_config& c) { return 4LL * c.head_dim; }
+int64_t cost_q(const arkv_config& c) {
+  int gs = c.group_size ? c.group_size : c.head_dim;
+  return 2LL * ((int64_t)c.head_dim * c.quant_bits / 8 + 8LL * (c.head_dim / gs));
+}
+
+arkv_status validate(const arkv_config* c) {
+  if (!c) return ARKV_ERR_INVALID_ARG;
+  if (c->n_layers <= 0 || c->n_q_heads <= 0 || c->n_kv_heads <= 0 || c->batch <= 0 || c->window <= 0)
+    return ARKV_ERR_CONFIG;
+  if (c->n_q_heads % c->n_kv_heads) return ARKV_ERR_CONFIG;
+  int G = c->n_q_heads / c->n_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return ARKV_ERR_CONFIG;
+  if (c->head_dim < 16 || c->head_dim > 256 || c->head_dim % 16) return ARKV_ERR_CONFIG;
+  if (c->quant_bits != 2 && c->quant_bits != 4 && c->quant_bits != 8) return ARKV_ERR_CONFIG;
+  int gs = c->group_size ? c->group_size : c->head_dim;
+  if (gs < 8 || gs % 8 || c->head_dim % gs) return ARKV_ERR_CONFIG;
+  if (c->budget_tokens <= 2 * c->window) return ARKV_ERR_CONFIG;  // R14
+  if (c->quant_mode != ARKV_QUANT_ASYM && c->quant_mode != ARKV_QUANT_SYM) return ARKV_ERR_CONFIG;
+  if (c->max_positions <= 0 || c->max_prompt <= 0 || c->max_prompt > c->max_positions) return ARKV_ERR_CONFIG;
+  if (c->alpha <= 0.0 || c->alpha > 1.0) return ARKV_ERR_CONFIG;
+  if (c->layout == ARKV_LAYOUT_FRAG && (c->quant_bits != 4 || c->head_dim % 32)) return ARKV_ERR_CONFIG;
+  if (c->layout < 0 || c->layout > 2) return ARKV_ERR_CONFIG;
+  if (c->decode_kernel < 0 || c->decode_kernel > 2) return ARKV_ERR_CONFIG;
+  return ARKV_OK;
+}
+
+Sizes compute_sizes(const arkv_config& c) {
+  Sizes s{};
+  Geom& g = s.g;
+  g.d = c.head_dim;
+  g.Hq = c.n_q_heads;
+  g.Hkv = c.n_kv_heads;
+  g.G = g.Hq / g.Hkv;
+  g.L = c.n_layers;
+  g.batch = c.batch;
+  g.W = c.window;
+  g.bits = c.quant_bits;
+  g.g = c.group_size ? c.group_size : c.head_dim;
+  g.ng = g.d / g.g;
+  g.mode = c.quant_mode;
+  g.layout = c.layout;
+  if (g.layout == ARKV_LAYOUT_AUTO)
+    g.layout = (c.quant_bits == 4 && c.head_dim % 32 == 0) ? ARKV_LAYOUT_FRAG : ARKV_LAYOUT_PLAIN;
+  g.B = c.budget_tokens;
+  g.cost_o = (int)cost_o(c);
+  g.cost_q = (int)cost_q(c);
+  g.tile_o = kTile * g.cost_o;
+  g.tile_q = kTile * g.cost_q;
+  const int64_t Bb = (int64_t)g.B * g.cost_o;
+  g.cap_o = (int)round_up(g.B + 1, kTile);
+  g.cap_q = (int)round_up((Bb - 2LL * g.W * g.cost_o) / g.cost_q + 1, kTile);
+  g.max_pos = c.max_positions;
+  g.n_units = g.batch * g.L * g.Hkv;
+  g.slot_bytes = round_up(Bb + g.tile_o + g.tile_q, 256);
+  g.meta_bytes = round_up((int64_t)g.cap_o * 12 + (int64_t)g.cap_q * 12, 256);
+  g.sm_scale = c.sm_scale > 0.f ? c.sm_scale : (float)(1.0 / std::sqrt((double)g.d));
+  g.gamma = (float)c.gamma;
+
+  s.n_spare = c.n_spare_slots > 0 ? c.n_spare_slots : g.batch * g.Hkv;
+  s.jobs_per_wave = std::min(s.n_spare, kMaxJobs);
+  s.max_splits = c.max_splits > 0 ? c.max_splits : 64;
+  s.n_chunks1 = (int)((c.max_prompt + kPfChunkHost - 1) / kPfChunkHost);
+  const int n_slots = g.n_units + s.n_spare;
+  s.off_meta = (int64_t)n_slots * g.slot_bytes;
+  s.off_desc = s.off_meta + (int64_t)n_slots * g.meta_bytes;
+  s.off_err = round_up(s.off_desc + (int64_t)g.n_units * sizeof(UnitDesc), 256);
+  s.arena = s.off_err + 256;
+
+  int64_t w = 0;
+  s.w_partials = w;
+  w = round_up(w + (int64_t)g.n_units * s.max_splits * g.G * (g.d + 2) * 4, 256);
+  s.w_logits = w;
+  w = round_up(w + (int64_t)g.n_units * g.G * (g.cap_o + g.cap_q) * 4, 256);
+  s.w_st = w;
+  const int64_t st_stride = std::max<int64_t>(g.max_pos, g.cap_o) + g.cap_q;
+  w = round_up(w + (int64_t)s.jobs_per_wave * st_stride, 256);
+  s.w_src = w;
+  w = round_up(w + (int64_t)s.jobs_per_wave * (g.cap_o + g.cap_q) * 4, 256);
+  s.w_pfp = w;
+  w = round_up(w + (int64_t)g.n_units * s.n_chunks1 * g.G * g.W * 8, 256);
+  s.w_accpf = w;
+  w = round_up(w + (int64_t)g.n_units * g.max_pos * 8, 256);
+  s.w_oq = w;
+  w = round_up(w + (int64_t)g.batch * g.L * 8, 256);
+  s.w_colsum = w;
+  w = round_up(w + (int64_t)g.batch * g.L * g.max_pos * 8, 256);
+  s.ws = w;
+  return s;
+}
+
+// Eq. 10 counts with the R14 headroom rule (must equal oracle.tailor_counts).
+void tailor_counts(const Geom& g, double alpha, int64_t K, double rho, int64_t* n_oe, int64_t* n_q) {
+  const int64_t W = g.W, B = g.B, Co = g.cost_o, Cq = g.cost_q, Bb = B * Co;
+  const int64_t n_e = K - W;
+  const int64_t b = (int64_t)std::floor(alpha * (double)n_e);
+  const int64_t quota = (int64_t)std::floor(rho * (double)(B - W));
+  int64_t o = std::min(std::min(quota, b), B - 2 * W);
+  int64_t q = std::min(b - o, (Bb - (o + 2 * W) * Co) / Cq);
+  *n_oe = o;
+  *n_q = q;
+}
+// Appends after which the unit first exceeds B_bytes (R12): the next tailor fires
+// at (position of the last counted token) + this.
+int64_t appends_to_trigger(const Geom& g, int64_t n_o, int64_t n_q) {
+  const int64_t Bb = (int64_t)g.B * g.cost_o;
+  const int64_t U = n_o * g.cost_o + n_q * g.cost_q;
+  return (Bb - U) / g.cost_o + 1;
+}
+
+bool check_cuda(cudaError_t e) { return e == cudaSuccess; }
+
+}  // namespace
+
+extern "C" {
+
+const char* arkv_version(void) { return "arkv 0.1 sm_100a layouts=plain,frag kernels=generic,mma-sync-prefill"; }
+
+const char* arkv_status_string(arkv_status s) {
+  switch (s) {
+    case ARKV_OK: return "ok";
+    case ARKV_ERR_INVALID_ARG: return "invalid argument";
+    case ARKV_ERR_CONFIG: return "invalid configuration";
+    case ARKV_ERR_SEQUENCE: return "sequencing error";
+    case ARKV_ERR_WINDOW: return "prompt shorter than W + 2 without rho_override";
+    case ARKV_ERR_LAYOUT: return "budget/bit-width differ from the cache";
+    case ARKV_ERR_CAPACITY: return "arena or workspace too small";
+    case ARKV_ERR_DEVICE: return "device error flag set";
+    case ARKV_ERR_CUDA: return "CUDA runtime error";
+    case ARKV_ERR_NO_DEVICE: return "no sm_100 device";
+  }
+  return "unknown";
+}
+
+arkv_status arkv_config_default(arkv_config* c) {
+  if (!c) return ARKV_ERR_INVALID_ARG;
+  std::memset(c, 0, sizeof(*c));
+  c->window = 32;
+  c->quant_bits = 4;
+  c->group_size = 0;
+  c->quant_mode = ARKV_QUANT_ASYM;
+  c->layout = ARKV_LAYOUT_AUTO;
+  c->alpha = 0.75;
+  c->tau[0] = 7.774;
+  c->tau[1] = 5.407;
+  c->tau[2] = 5.528;
+  c->gamma = 263.81;
+  c->stat_eps = 1e-30;
+  c->batch = 1;
+  return ARKV_OK;
+}
+
+arkv_status arkv_cache_bytes(const arkv_config* cfg, size_t* arena_bytes, size_t* workspace_bytes) {
+  arkv_status st = validate(cfg);
+  if (st != ARKV_OK) return st;
+  Sizes s = compute_sizes(*cfg);
+  if (arena_bytes) *arena_bytes = (size_t)s.arena;
+  if (workspace_bytes) *workspace_bytes = (size_t)s.ws;
+  return ARKV_OK;
+}
+
+arkv_status arkv_schedule(const arkv_config* cfg, int32_t P, double rho, int32_t n_steps, int32_t* events,
+                          int32_t max_events, int32_t* n_events) {
+  arkv_status st = validate(cfg);
+  if (st != ARKV_OK) return st;
+  if (!n_events || P <= 0 || n_steps < 0) return ARKV_ERR_INVALID_ARG;
+  Geom g = compute_sizes(*cfg).g;
+  int n = 0;
+  auto push = [&](int s, int64_t a, int64_t b, int64_t c) {
+    if (events && n < max_events) {
+      events[4 * n + 0] = s;
+      events[4 * n + 1] = (int32_t)a;
+      events[4 * n + 2] = (int32_t)b;
+      events[4 * n + 3] = (int32_t)c;
+    }
+    ++n;
+  };
+  int64_t n_o, n_q;
+  if (P > g.B - g.W) {
+    int64_t oe, q;
+    tailor_counts(g, cfg->alpha, P, rho, &oe, &q);
+    push(-1, oe + g.W, q, P - g.W - oe - q);
+    n_o = oe + g.W;
+    n_q = q;
+  } else {
+    n_o = P;
+    n_q = 0;
+  }
+  // drive by trigger positions, exactly as the runtime does
+  int64_t trig = (P - 1) + appends_to_trigger(g, n_o, n_q);
+  for (int s = 0; s < n_steps; ++s) {
+    const int64_t t = P + s;
+    if (t == trig) {
+      const int64_t K = n_o + 1 + n_q;
+      int64_t oe, q;
+      tailor_counts(g, cfg->alpha, K, rho, &oe, &q);
+      push(s, oe + g.W, q, K - g.W - oe - q);
+      n_o = oe + g.W;
+      n_q = q;
+      trig = t + appends_to_trigger(g, n_o, n_q);
+    } else {
+      n_o += 1;
+    }
+  }
+  *n_events = n;
+  return ARKV_OK;
+}
+
+arkv_status arkv_oq_score(const arkv_config* cfg, double H, double m2, double m4, double* stats3, double* score) {
+  if (!cfg) return ARKV_ERR_INVALID_ARG;
+  const double eps = cfg->stat_eps;
+  double K = m2 > eps ? m4 / (m2 * m2) : 1.0;
+  double Hc = std::fmax(H, eps), Vc = std::fmax(m2, eps), Kc = std::fmax(K, eps);
+  if (stats3) {
+    stats3[0] = Hc;
+    stats3[1] = Vc;
+    stats3[2] = Kc;
+  }
+  if (score) *score = std::pow(Hc, 1.0 / cfg->tau[0]) * std::pow(Vc, 1.0 / cfg->tau[1]) * std::pow(Kc, 1.0 / cfg->tau[2]);
+  return ARKV_OK;
+}
+
+arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t arena_bytes, void* d_workspace,
+                              size_t workspace_bytes, arkv_cache** out) {
+  arkv_status st = validate(cfg);
+  if (st != ARKV_OK) return st;
+  if (!d_arena || !d_workspace || !out) return ARKV_ERR_INVALID_ARG;
+  if (((uintptr_t)d_arena & 255) || ((uintptr_t)d_workspace & 255)) return ARKV_ERR_INVALID_ARG;
+  Sizes s = compute_sizes(*cfg);
+  if ((int64_t)arena_bytes < s.arena || (int64_t)workspace_bytes < s.ws) return ARKV_ERR_CAPACITY;
+  int dev = 0;
+  if (!check_cuda(cudaGetDevice(&dev))) return ARKV_ERR_NO_DEVICE;
+  cudaDeviceProp prop;
+  if (!check_cuda(cudaGetDeviceProperties(&prop, dev))) return ARKV_ERR_NO_DEVICE;
+  if (prop.major != 10) return ARKV_ERR_NO_DEVICE;
+  arkv_cache* c = new arkv_cache();
+  c->cfg = *cfg;
+  c->g = s.g;
+  c->device = dev;
+  uint8_t* a = (uint8_t*)d_arena;
+  c->slots = a;
+  c->meta = a + s.off_meta;
+  c->desc = (UnitDesc*)(a + s.off_desc);
+  c->err = (int32_t*)(a + s.off_err);
+  c->n_spare = s.n_spare;
+  c->n_slots = s.g.n_units + s.n_spare;
+  uint8_t* w = (uint8_t*)d_workspace;
+  c->partials = (float*)(w + s.w_partials);
+  c->logits = (float*)(w + s.w_logits);
+  c->st_scratch = (int8_t*)(w + s.w_st);
+  c->src_scratch = (int32_t*)(w + s.w_src);
+  c->pf_partials = (float*)(w + s.w_pfp);
+  c->acc_pf = (float2*)(w + s.w_accpf);
+  c->oq_tmp = (double*)(w + s.w_oq);
+  c->colsum = (double*)(w + s.w_colsum);
+  c->jobs_per_wave = s.jobs_per_wave;
+  c->max_splits = s.max_splits;
+  c->n_chunks1_max = s.n_chunks1;
+  const int BL = s.g.batch * s.g.L;
+  c->rho.assign(BL, 1.0);
+  c->n_o.assign(BL, 0);
+  c->n_q.assign(BL, 0);
+  c->t_next.assign(BL, 0);
+  c->trig.assign(BL, 0);
+  c->unit_slot.resize(s.g.n_units);
+  for (int u = 0; u < s.g.n_units; ++u) c->unit_slot[u] = u;
+  for (int k = c->n_slots - 1; k >= s.g.n_units; --k) c->spare.push_back(k);
+  bool fast_ok = s.g.layout == ARKV_LAYOUT_FRAG && s.g.bits == 4 && s.g.d == 128;
+  c->fast = cfg->decode_kernel == 2 ? fast_ok : (cfg->decode_kernel == 0 ? fast_ok : false);
+  if (cfg->decode_kernel == 2 && !fast_ok) {
+    delete c;
+    return ARKV_ERR_CONFIG;
+  }
+  if (!check_cuda(cudaMemset(c->err, 0, 4))) {
+    delete c;
+    return ARKV_ERR_CUDA;
+  }
+  *out = c;
+  return ARKV_OK;
+}
+
+arkv_status arkv_cache_destroy(arkv_cache* c) {
+  if (c)
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  delete c;
+  return ARKV_OK;
+}
+
+arkv_status arkv_profile(arkv_cache* c, int32_t enable) {
+  if (!c) return ARKV_ERR_INVALID_ARG;
+  c->prof = enable != 0;
+  c->ev_used = 0;
+  if (c->prof && c->ev.empty()) {
+    const int pairs = 8192;
+    c->ev.resize(2 * pairs);
+    c->ev_bytes.assign(pairs, 0.0);
+    for (auto& e : c->ev)
+      if (!check_cuda(cudaEventCreate(&e))) return ARKV_ERR_CUDA;
+  }
+  return ARKV_OK;
+}
+
+arkv_status arkv_profile_read(arkv_cache* c, int32_t which, double* total_ms, int64_t* launches, double* alg_bytes) {
+  if (!c || which != 0) return ARKV_ERR_INVALID_ARG;
+  double ms = 0.0, by = 0.0;
+  for (int i = 0; i < c->ev_used; ++i) {
+    if (!check_cuda(cudaEventSynchronize(c->ev[2 * i + 1]))) return ARKV_ERR_CUDA;
+    float t = 0.f;
+    if (!check_cuda(cudaEventElapsedTime(&t, c->ev[2 * i], c->ev[2 * i + 1]))) return ARKV_ERR_CUDA;
+    ms += t;
+    by += c->ev_bytes[i];
+  }
+  if (total_ms) *total_ms = ms;
+  if (launches) *launches = c->ev_used;
+  if (alg_bytes) *alg_bytes = by;
+  return ARKV_OK;
+}
+
+int64_t arkv_launch_count(const arkv_cache* c) { return c ? c->launches : 0; }
+
+// Runs a list of tailor jobs in waves bounded by the spare-slot count.
+static arkv_status run_jobs(arkv_cache* c, std::vector<TailorJob>& jobs, const uint16_t* pk, const uint16_t* pv, int P,
+                            cudaStream_t s) {
+  const Geom& g = c->g;
+  size_t i = 0;
+  while (i < jobs.size()) {
+    const int n = (int)std::min<size_t>(jobs.size() - i, (size_t)c->jobs_per_wave);
+    TailorJobs tj;
+    std::memset(&tj, 0, sizeof(tj));
+    int max_tiles = 1;
+    for (int k = 0; k < n; ++k) {
+      TailorJob jb = jobs[i + k];
+      if (jb.new_slot < 0) {
+        if (c->spare.empty()) return ARKV_ERR_CAPACITY;
+        jb.new_slot = c->spare.back();
+        c->spare.pop_back();
+      }
+      jobs[i + k] = jb;
+      tj.j[k] = jb;
+      int no = jb.n_oe + jb.n_win_old;
+      int tiles = (no + kTile - 1) / kTile + (jb.n_q_new + kTile - 1) / kTile;
+      max_tiles = std::max(max_tiles, tiles);
+      if (no > g.cap_o + 0 || jb.n_q_new > g.cap_q) return ARKV_ERR_CAPACITY;
+    }
+    int nl = launch_tailor(g, tj, n, max_tiles, c->slots, c->meta, c->desc, pk, pv, P, c->acc_pf, c->st_scratch,
+                           c->src_scratch, c->err, s);
+    if (nl < 0) return ARKV_ERR_CONFIG;
+    c->launches += nl;
+    if (!check_cuda(cudaGetLastError())) return ARKV_ERR_CUDA;
+    for (int k = 0; k < n; ++k) {
+      const TailorJob& jb = jobs[i + k];
+      if (jb.old_slot >= 0) c->spare.push_back(jb.old_slot);
+      c->unit_slot[jb.unit] = jb.new_slot;
+    }
+    i += n;
+  }
+  return ARKV_OK;
+}
+
+arkv_status arkv_prefill_begin(arkv_cache* c, const void* q_win, const void* k, int32_t P, double* d_colsum,
+                               void* stream) {
+  if (!c || !q_win || !k) return ARKV_ERR_INVALID_ARG;
+  if (c->prefilled) return ARKV_ERR_SEQUENCE;
+  const Geom& g = c->g;
+  if (P <= 0 || P > c->cfg.max_prompt || P >= g.max_pos) return ARKV_ERR_INVALID_ARG;
+  if (P < g.W + 2) return ARKV_ERR_WINDOW;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n_chunks1 = (P + kPfChunkHost - 1) / kPfChunkHost;
+  int nl = launch_prefill_begin(g, (const uint16_t*)q_win, (const uint16_t*)k, P, c->pf_partials, n_chunks1, c->acc_pf,
+                                d_colsum ? d_colsum : c->colsum, s);
+  if (nl < 0) return ARKV_ERR_CONFIG;
+  c->launches += nl;
+  if (!check_cuda(cudaGetLastError())) return ARKV_ERR_CUDA;
+  return ARKV_OK;
+}
+
+arkv_status arkv_prefill_finish(arkv_cache* c, const void* k, const void* v, int32_t P, const double* d_colsum,
+                                const double* rho_override, double* d_stats, double* d_oq, double* h_rho,
+                                void* stream) {
+  if (!c || !k || !v) return ARKV_ERR_INVALID_ARG;
+  if (c->prefilled) return ARKV_ERR_SEQUENCE;
+  const Geom& g = c->g;
+  if (P <= 0 || P > c->cfg.max_prompt || P >= g.max_pos) return ARKV_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool tailor = P > g.B - g.W;  // R14
+  const bool stats_ok = P >= g.W + 2;
+  if (!stats_ok && (rho_override == nullptr || tailor)) return ARKV_ERR_WINDOW;
+  const int BL = g.batch * g.L;
+  std::vector<double> rho(BL, 1.0);
+  if (stats_ok) {
+    double* oq = d_oq ? d_oq : c->oq_tmp;
+    int nl = launch_prefill_finish(g, d_colsum ? d_colsum : c->colsum, P, d_stats, oq, c->cfg.tau, c->cfg.stat_eps, s);
+    c->launches += nl;
+    if (!check_cuda(cudaGetLastError())) return ARKV_ERR_CUDA;
+    std::vector<double> h(BL);
+    if (!check_cuda(cudaMemcpyAsync(h.data(), oq, BL * sizeof(double), cudaMemcpyDeviceToHost, s))) return ARKV_ERR_CUDA;
+    if (!check_cuda(cudaStreamSynchronize(s))) return ARKV_ERR_CUDA;
+    for (int b = 0; b < g.batch; ++b) {  // Eq. 7: ratio within the sequence (R8)
+      double mx = 0.0;
+      for (int l = 0; l < g.L; ++l) mx = std::max(mx, h[b * g.L + l]);
+      for (int l = 0; l < g.L; ++l) rho[b * g.L + l] = mx > 0.0 ? h[b * g.L + l] / mx : 1.0;
+    }
+  }
+  if (rho_override)
+    for (int i = 0; i < BL; ++i) rho[i] = rho_override[i];
+  c->rho = rho;
+  if (h_rho)
+    for (int i = 0; i < BL; ++i) h_rho[i] = rho[i];
+
+  // ingest (+ prefill-end tailor)
+  std::vector<TailorJob> jobs;
+  for (int bl = 0; bl < BL; ++bl) {
+    int64_t oe, q;
+    int n_win, n_o;
+    if (tailor) {
+      tailor_counts(g, c->cfg.alpha, P, rho[bl], &oe, &q);
+      n_win = g.W;
+      n_o = (int)oe + g.W;
+    } else {
+      n_win = std::min(g.W, P);
+      oe = P - n_win;
+      q = 0;
+      n_o = P;
+    }
+    c->n_o[bl] = n_o;
+    c->n_q[bl] = (int)q;
+    c->t_next[bl] = P;
+    c->trig[bl] = (int)((P - 1) + appends_to_trigger(g, n_o, q));
+    for (int kvh = 0; kvh < g.Hkv; ++kvh) {
+      TailorJob jb{};
+      jb.unit = bl * g.Hkv + kvh;
+      jb.old_slot = -1;
+      jb.new_slot = c->unit_slot[jb.unit];
+      jb.n_o_old = P;
+      jb.n_q_old = 0;
+      jb.n_win_old = n_win;
+      jb.n_oe = (int)oe;
+      jb.n_q_new = (int)q;
+      jb.trig_new = c->trig[bl];
+      jb.t_next = P;
+      jb.identity = tailor ? 0 : 1;
+      jobs.push_back(jb);
+    }
+  }
+  arkv_status st = run_jobs(c, jobs, (const uint16_t*)k, (const uint16_t*)v, P, s);
+  if (st != ARKV_OK) return st;
+  c->prefilled = true;
+  return ARKV_OK;
+}
+
+arkv_status arkv_prefill_stats(arkv_cache* c, const void* q_win, const void* k, const void* v, int32_t P,
+                               const double* rho_override, double* d_stats, double* d_oq, double* h_rho,
+                               void* stream) {
+  if (!c || !k || !v) return ARKV_ERR_INVALID_ARG;
+  if (P >= c->g.W + 2) {
+    arkv_status st = arkv_prefill_begin(c, q_win, k, P, nullptr, stream);
+    if (st != ARKV_OK) return st;
+  }
+  return arkv_prefill_finish(c, k, v, P, nullptr, rho_override, d_stats, d_oq, h_rho, stream);
+}
+
+arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, const void* q, const void* k,
+                             const void* v, int32_t budget_tokens, int32_t quant_bits, void* out, int32_t out_fp32,
+                             void* stream) {
+  if (!c || !q || !k || !v || !out) return ARKV_ERR_INVALID_ARG;
+  const Geom& g = c->g;
+  if (layer0 < 0 || n_layers <= 0 || layer0 + n_layers > g.L) return ARKV_ERR_INVALID_ARG;
+  if (budget_tokens != g.B || quant_bits != g.bits) return ARKV_ERR_LAYOUT;
+  if (!c->prefilled) return ARKV_ERR_SEQUENCE;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<TailorJob> jobs;
+  int max_tiles = 1;
+  for (int b = 0; b < g.batch; ++b)
+    for (int l = layer0; l < layer0 + n_layers; ++l) {
+      const int bl = b * g.L + l;
+      const int t = c->t_next[bl];
+      if (t + 1 > g.max_pos) return ARKV_ERR_SEQUENCE;
+      if (t == c->trig[bl]) {
+        const int64_t K = (int64_t)c->n_o[bl] + 1 + c->n_q[bl];
+        int64_t oe, qn;
+        tailor_counts(g, c->cfg.alpha, K, c->rho[bl], &oe, &qn);
+        const int n_o_after = (int)oe + g.W;  // after this step's append
+        const int trig_new = (int)(t + appends_to_trigger(g, n_o_after, qn));
+        for (int kvh = 0; kvh < g.Hkv; ++kvh) {
+          TailorJob jb{};
+          jb.unit = bl * g.Hkv + kvh;
+          jb.old_slot = c->unit_slot[jb.unit];
+          jb.new_slot = -1;
+          jb.n_o_old = c->n_o[bl];
+          jb.n_q_old = c->n_q[bl];
+          jb.n_win_old = g.W - 1;
+          jb.n_oe = (int)oe;
+          jb.n_q_new = (int)qn;
+          jb.trig_new = trig_new;
+          jb.t_next = t;
+          jb.identity = 0;
+          jobs.push_back(jb);
+        }
+        c->n_o[bl] = n_o_after - 1;
+        c->n_q[bl] = (int)qn;
+        c->trig[bl] = trig_new;
+      }
+      const int tiles = (c->n_o[bl] + 1 + kTile - 1) / kTile + (c->n_q[bl] + kTile - 1) / kTile;
+      max_tiles = std::max(max_tiles, tiles);
+    }
+  if (!jobs.empty()) {
+    arkv_status st = run_jobs(c, jobs, nullptr, nullptr, 0, s);
+    if (st != ARKV_OK) return st;
+  }
+  // split-K fan-out: ~4 CTAs per SM in flight, never more splits than tiles
+  const int n_units_call = g.batch * n_layers * g.Hkv;
+  int S = (4 * 148 + n_units_call - 1) / n_units_call;
+  S = std::max(1, std::min(S, std::min(c->max_splits, max_tiles)));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->prof && 2 * (c->ev_used + 1) <= (int)c->ev.size()) {
+    e0 = c->ev[2 * c->ev_used];
+    e1 = c->ev[2 * c->ev_used + 1];
+    // algorithmic bytes of this launch: cache segments read + the step's token read and
+    // appended + the query read
+    double by = 0.0;
+    for (int b = 0; b < g.batch; ++b)
+      for (int l = layer0; l < layer0 + n_layers; ++l) {
+        const int bl = b * g.L + l;
+        by += (double)g.Hkv * ((double)c->n_o[bl] * g.cost_o + (double)c->n_q[bl] * g.cost_q + 2.0 * g.cost_o +
+                               2.0 * g.G * g.d);
+      }
+    c->ev_bytes[c->ev_used] = by;
+    c->ev_used++;
+  }
+  int nl = launch_decode(g, layer0, n_layers, (const uint16_t*)q, (const uint16_t*)k, (const uint16_t*)v, out,
+                         out_fp32, c->slots, c->meta, c->desc, c->partials, c->logits, S, c->max_splits, c->fast ? 1 : 0,
+                         c->err, s, e0, e1);
+  if (nl < 0 && c->fast) {  // fast kernel not available for this shape: generic kernel
+    nl = launch_decode(g, layer0, n_layers, (const uint16_t*)q, (const uint16_t*)k, (const uint16_t*)v, out, out_fp32,
+                       c->slots, c->meta, c->desc, c->partials, c->logits, S, c->max_splits, 0, c->err, s, e0, e1);
+  }
+  if (nl < 0) return ARKV_ERR_CONFIG;
+  c->launches += nl;
+  if (!check_cuda(cudaGetLastError())) return ARKV_ERR_CUDA;
+  for (int b = 0; b < g.batch; ++b)
+    for (int l = layer0; l < layer0 + n_layers; ++l) {
+      const int bl = b * g.L + l;
+      c->n_o[bl] += 1;
+      c->t_next[bl] += 1;
+    }
+  return ARKV_OK;
+}
+
+arkv_status arkv_unit_counts(const arkv_cache* c, int32_t b, int32_t l, int32_t* n_o, int32_t* n_q, int32_t* next_pos,
+                             int32_t* next_tailor) {
+  if (!c || b < 0 || b >= c->g.batch || l < 0 || l >= c->g.L) return ARKV_ERR_INVALID_ARG;
+  const int bl = b * c->g.L + l;
+  if (n_o) *n_o = c->n_o[bl];
+  if (n_q) *n_q = c->n_q[bl];
+  if (next_pos) *next_pos = c->t_next[bl];
+  if (next_tailor) *next_tailor = c->trig[bl];
+  return ARKV_OK;
+}
+
+arkv_status arkv_export_unit(arkv_cache* c, int32_t b, int32_t l, int32_t kvh, arkv_unit_export* out, void* stream) {
+  if (!c || !out || b < 0 || b >= c->g.batch || l < 0 || l >= c->g.L || kvh < 0 || kvh >= c->g.Hkv)
+    return ARKV_ERR_INVALID_ARG;
+  const Geom& g = c->g;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int u = (b * g.L + l) * g.Hkv + kvh;
+  UnitDesc dsc;
+  if (!check_cuda(cudaMemcpyAsync(&dsc, c->desc + u, sizeof(dsc), cudaMemcpyDeviceToHost, s))) return ARKV_ERR_CUDA;
+  if (!check_cuda(cudaStreamSynchronize(s))) return ARKV_ERR_CUDA;
+  std::vector<uint8_t> slot(g.slot_bytes), meta(g.meta_bytes);
+  if (!check_cuda(cudaMemcpyAsync(slot.data(), c->slots + (int64_t)dsc.slot * g.slot_bytes, g.slot_bytes,
+                                  cudaMemcpyDeviceToHost, s)))
+    return ARKV_ERR_CUDA;
+  if (!check_cuda(cudaMemcpyAsync(meta.data(), c->meta + (int64_t)dsc.slot * g.meta_bytes, g.meta_bytes,
+                                  cudaMemcpyDeviceToHost, s)))
+    return ARKV_ERR_CUDA;
+  if (!check_cuda(cudaStreamSynchronize(s))) return ARKV_ERR_CUDA;
+  SlotMeta sm = slot_meta(meta.data(), g, 0);
+  const int n_pos = dsc.t_next;
+  if (out->n_pos < n_pos) return ARKV_ERR_CAPACITY;
+  out->n_o = dsc.n_o;
+  out->n_q = dsc.n_q;
+  const int d = g.d, ng = g.ng;
+  const int off = g.mode == ARKV_QUANT_SYM ? (1 << (g.bits - 1)) : 0;
+  if (out->state) {
+    for (int p = 0; p < out->n_pos; ++p) out->state[p] = p < n_pos ? 3 : 0;
+  }
+  for (int r = 0; r < dsc.n_o; ++r) {
+    const int p = sm.pos_o[r];
+    if (p < 0 || p >= n_pos) return ARKV_ERR_DEVICE;
+    if (out->state) out->state[p] = 1;
+    const uint8_t* tb = o_tile_ptr(slot.data(), g, r / kTile);
+    for (int x = 0; x < d; ++x) {
+      if (out->o_k) out->o_k[(int64_t)p * d + x] = *(const uint16_t*)(tb + o_k_off(g, r % kTile, x));
+      if (out->o_v) out->o_v[(int64_t)p * d + x] = *(const uint16_t*)(tb + o_v_off(g, r % kTile, x));
+    }
+  }
+  for (int r = 0; r < dsc.n_q; ++r) {
+    const int p = sm.pos_q[r];
+    if (p < 0 || p >= n_pos) return ARKV_ERR_DEVICE;
+    if (out->state) out->state[p] = 2;
+    const uint8_t* tb = q_tile_ptr(slot.data(), g, r / kTile);
+    const int j = r % kTile;
+    for (int x = 0; x < d; ++x) {
+      int byte, shift;
+      q_k_loc(g, j, x, &byte, &shift);
+      int ck = (int)((tb[byte] >> shift) & ((1u << g.bits) - 1u)) - off;
+      q_v_loc(g, j, x, &byte, &shift);
+      int cv = (int)((tb[byte] >> shift) & ((1u << g.bits) - 1u)) - off;
+      if (out->q_k) out->q_k[(int64_t)p * d + x] = (int16_t)ck;
+      if (out->q_v) out->q_v[(int64_t)p * d + x] = (int16_t)cv;
+    }
+    for (int gi = 0; gi < ng; ++gi) {
+      if (out->k_scale) out->k_scale[(int64_t)p * ng + gi] = *(const float*)(tb + q_sc_off(g, j, 0, gi));
+      if (out->k_zero) out->k_zero[(int64_t)p * ng + gi] = *(const float*)(tb + q_sc_off(g, j, 1, gi));
+      if (out->v_scale) out->v_scale[(int64_t)p * ng + gi] = *(const float*)(tb + q_sc_off(g, j, 2, gi));
+      if (out->v_zero) out->v_zero[(int64_t)p * ng + gi] = *(const float*)(tb + q_sc_off(g, j, 3, gi));
+    }
+  }
+  return ARKV_OK;
+}
+
+arkv_status arkv_check(arkv_cache* c, void* stream) {
+  if (!c) return ARKV_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!check_cuda(cudaStreamSynchronize(s))) return ARKV_ERR_CUDA;
+  int32_t e = 0;
+  if (!check_cuda(cudaMemcpy(&e, c->err, 4, cudaMemcpyDeviceToHost))) return ARKV_ERR_CUDA;
+  if (e) {
+    cudaMemset(c->err, 0, 4);
+    std::fprintf(stderr, "arkv: device error flag 0x%x\n", e);
+    return ARKV_ERR_DEVICE;
+  }
+  return ARKV_OK;
+}
+
+}  // extern "C"

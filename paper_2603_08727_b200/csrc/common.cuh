@@ -1,0 +1,158 @@
+// common.cuh — geometry, device descriptors and the HBM tile layouts of the ARKV cache.
+//
+// A "unit" is one (sequence, layer, KV head).  Its tokens live in one arena SLOT of
+// slot_bytes, used as a two-stack: 32-token Original tiles grow up from
+// offset 0, 32-token Quantized tiles grow down from the end.  Eq. 1's byte budget
+// (R10) bounds n_o*C_o + n_q*C_q <= B_bytes + C_o, so the stacks never
+// meet in a slot of B_bytes + C_o + one tile of each kind.
+//
+// Two tile layouts:
+//   PLAIN — token rows: O row = K[d] bf16 | V[d] bf16; Q row = K codes | V codes |
+//           k_scale[ng] | k_zero[ng] | v_scale[ng] | v_zero[ng] (fp32).
+//   FRAG  — "fragment-native": every 16-byte vector a lane loads is exactly the
+//           register fragment of an mma.sync.m16n8k16 operand (K rows as the A
+//           operand of QK^T, V transposed as the A operand of PV), so the fast
+//           decode kernel streams tiles with fully coalesced 128-bit loads and no
+//           shared-memory transposes.  Q tiles store 4-bit codes nibble-interleaved
+//           for the fp16 "magic number" unpack (one LOP3 per two codes).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/arkv.h"
+
+namespace arkv {
+
+constexpr int kTile = 32;  // tokens per tile
+
+// Device error flag bits (arkv_check).
+enum : int32_t { kErrNonFinite = 1, kErrCapacity = 2, kErrIntegrity = 4 };
+
+struct Geom {
+  int32_t d, G, Hq, Hkv, L, batch, W, bits, g, ng, mode, layout;
+  int32_t B;                      // budget tokens
+  int32_t cost_o, cost_q;         // bytes per token (Eq. 1 C_orig, C_quant; R10)
+  int32_t tile_o, tile_q;         // bytes per 32-token tile
+  int32_t cap_o, cap_q;           // row capacity of the per-slot metadata (multiples of 32)
+  int32_t max_pos, n_units;
+  int64_t slot_bytes;             // bytes per slot (two-stack)
+  int64_t meta_bytes;             // per-slot metadata: pos_o, pos_q, acc_o, acc_q
+  float sm_scale, gamma;
+};
+
+struct __align__(32) UnitDesc {
+  int32_t slot;    // arena slot of the unit's tiles
+  int32_t n_o;     // Original rows (window included; excludes the token of the running step)
+  int32_t n_q;     // Quantized rows
+  int32_t t_next;  // position of the next appended token
+  int32_t trig;    // position of the next tailor (R12, R15)
+  int32_t pad0, pad1, pad2;
+};
+
+// ---------------------------------------------------------------------------------
+// Slot addressing
+// ---------------------------------------------------------------------------------
+__host__ __device__ inline uint8_t* o_tile_ptr(uint8_t* slot, const Geom& g, int tile) {
+  return slot + (int64_t)tile * g.tile_o;
+}
+__host__ __device__ inline uint8_t* q_tile_ptr(uint8_t* slot, const Geom& g, int tile) {
+  return slot + g.slot_bytes - (int64_t)(tile + 1) * g.tile_q;
+}
+struct SlotMeta {
+  int32_t* pos_o;
+  int32_t* pos_q;
+  float2* acc_o;
+  float2* acc_q;
+};
+__host__ __device__ inline SlotMeta slot_meta(uint8_t* meta_base, const Geom& g, int slot) {
+  uint8_t* m = meta_base + (int64_t)slot * g.meta_bytes;
+  SlotMeta s;
+  s.pos_o = (int32_t*)m;
+  s.pos_q = s.pos_o + g.cap_o;
+  s.acc_o = (float2*)(s.pos_q + g.cap_q);
+  s.acc_q = s.acc_o + g.cap_o;
+  return s;
+}
+
+// ---------------------------------------------------------------------------------
+// Tile layouts: byte offset of element (token j in [0,32), dim x in [0,d)) in a tile.
+// ---------------------------------------------------------------------------------
+// Offset of per-lane word k of lane `lane` in a "lane word stream" block: lanes'
+// words are grouped in quads so one 128-bit load per lane reads four consecutive
+// words of that lane and a warp-wide load is one contiguous 512-byte segment.
+__host__ __device__ inline int lane_word(int k, int lane) { return (((k >> 2) * 32 + lane) << 2) + (k & 3); }
+
+// O tile, K element (bf16).
+__host__ __device__ inline int o_k_off(const Geom& g, int j, int x) {
+  if (g.layout != ARKV_LAYOUT_FRAG) return (j * 2 * g.d + x) * 2;
+  // A operand of S = K q^T (m16n8k16, M = tokens): thread (gg,t) holds rows gg, gg+8
+  // of each 16-token m-tile and, per 16-dim chunk c, dims t*(d/4)+4c+{0,1} (R0/R1)
+  // and t*(d/4)+4c+{2,3} (R2/R3).
+  int mt = j >> 4, jj = j & 15, h = jj >> 3, gg = jj & 7;
+  int q4 = g.d >> 2;
+  int t = x / q4, rem = x % q4, c = rem >> 2, e = rem & 3;
+  int lane = 4 * gg + t;
+  int k = ((mt * 2 + h) * (g.d >> 4) + c) * 2 + (e >> 1);
+  return lane_word(k, lane) * 4 + (e & 1) * 2;
+}
+// O tile, V element (bf16).
+__host__ __device__ inline int o_v_off(const Geom& g, int j, int x) {
+  if (g.layout != ARKV_LAYOUT_FRAG) return (j * 2 * g.d + g.d + x) * 2;
+  // A operand of O^T = V^T P^T (M = dims, K = tokens): thread (gg,t) holds dim rows
+  // gg (sel 0) / gg+8 (sel 1) of each 16-dim m-tile and tokens 2t,2t+1 (hi 0) /
+  // 2t+8,2t+9 (hi 1) of each 16-token k-step kc; register R = sel + 2 hi.
+  int mtv = x >> 4, r = x & 15, gg = r & 7, sel = r >> 3;
+  int kc = j >> 4, jj = j & 15, hi = jj >> 3, tt = jj & 7, t = tt >> 1, u = tt & 1;
+  int lane = 4 * gg + t;
+  int k = (mtv * 2 + kc) * 4 + sel + 2 * hi;
+  return 64 * g.d + lane_word(k, lane) * 4 + u * 2;
+}
+
+// Q tile codes: returns the byte offset of the byte holding the code and its bit shift.
+__host__ __device__ inline void q_k_loc(const Geom& g, int j, int x, int* byte, int* shift) {
+  if (g.layout != ARKV_LAYOUT_FRAG) {
+    int bit = x * g.bits;
+    *byte = j * g.cost_q + (bit >> 3);
+    *shift = bit & 7;
+    return;
+  }
+  // 4-bit, d % 32 == 0.  Word (row, t, jp) nibble e holds dim 32 jp + 8 t + e.
+  int mt = j >> 4, jj = j & 15, h = jj >> 3, gg = jj & 7;
+  int jp = x >> 5, t = (x >> 3) & 3, e = x & 7;
+  int lane = 4 * gg + t;
+  int k = (mt * 2 + h) * (g.d >> 5) + jp;
+  int w = lane_word(k, lane);
+  *byte = w * 4 + (e >> 1);
+  *shift = (e & 1) * 4;
+}
+__host__ __device__ inline void q_v_loc(const Geom& g, int j, int x, int* byte, int* shift) {
+  if (g.layout != ARKV_LAYOUT_FRAG) {
+    int bit = x * g.bits;
+    *byte = j * g.cost_q + (g.d * g.bits >> 3) + (bit >> 3);
+    *shift = bit & 7;
+    return;
+  }
+  // V transposed: word (dim row, t) nibble e holds token (kc*16 + hi*8 + 2t + u)
+  // with e = 2 kc + hi + 4 u.
+  int mtv = x >> 4, r = x & 15, gg = r & 7, sel = r >> 3;
+  int kc = j >> 4, jj = j & 15, hi = jj >> 3, tt = jj & 7, t = tt >> 1, u = tt & 1;
+  int e = 2 * kc + hi + 4 * u;
+  int lane = 4 * gg + t;
+  int k = mtv * 2 + sel;
+  int w = (g.d >> 3) * 32 + lane_word(k, lane);  // after the K block (16 d bytes = 4 d words)
+  *byte = w * 4 + (e >> 1);
+  *shift = (e & 1) * 4;
+}
+// which: 0 k_scale, 1 k_zero, 2 v_scale, 3 v_zero.
+__host__ __device__ inline int q_sc_off(const Geom& g, int j, int which, int grp) {
+  if (g.layout != ARKV_LAYOUT_FRAG) return j * g.cost_q + 2 * (g.d * g.bits >> 3) + (which * g.ng + grp) * 4;
+  return 32 * g.d + ((which * g.ng + grp) * 32 + j) * 4;
+}
+
+__device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+__device__ __forceinline__ uint16_t f_to_bf16_rne(float f) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+}  // namespace arkv

@@ -1,0 +1,374 @@
+// k_decode.cu — decode attention over O ∪ Q (D1, D3, D7 of DESIGN.md §2).
+//
+// Split-K (flash-decoding) over each unit's 32-token tiles: split s of S takes an
+// equal share of the unit's Original tiles and of its Quantized tiles, so every
+// split streams the same bytes.  Each CTA appends the step's token (D1) if it owns
+// the last Original tile, runs an online softmax over its tiles (Quantized tokens
+// are dequantized in registers: x̃ = code·s + z), and writes a partial
+// (m, l, o).  The combine kernel merges the partials, writes the output, performs
+// the heavy-hitter accumulation acc1 += Σ_h p, acc2 += Σ_h p² of the W steps before
+// the next tailor (Eq. 9 / R19) from the logits the split kernel kept, and advances
+// the unit descriptor.  This generic kernel handles every layout/shape; the fast
+// tensor-core kernel (k_decode_fast.cu) takes FRAG-layout 4-bit d=128 caches.
+#include "kernels.h"
+
+namespace arkv {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void unit_of(const DecodeArgs& a, int ul, int& b, int& li, int& kvh, int& u) {
+  const Geom& g = a.g;
+  b = ul / (a.n_layers * g.Hkv);
+  int rem = ul % (a.n_layers * g.Hkv);
+  li = rem / g.Hkv;
+  kvh = rem % g.Hkv;
+  u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
+}
+
+__device__ __forceinline__ void bf16x8_to_f(uint4 w, float (&f)[8]) {
+  uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(ww[i] << 16);
+    f[2 * i + 1] = __uint_as_float(ww[i] & 0xFFFF0000u);
+  }
+}
+
+// Generic split kernel.  LG lanes per token, each lane owns 8 consecutive dims.
+template <int G, int LG>
+__global__ void __launch_bounds__(128) decode_split_generic(DecodeArgs a) {
+  constexpr int TPP = 32 / LG;  // tokens per warp pass
+  const Geom& g = a.g;
+  const int d = g.d;
+  int b, li, kvh, u;
+  unit_of(a, blockIdx.y, b, li, kvh, u);
+  const UnitDesc dsc = a.desc[u];
+  uint8_t* slot = a.slots + (int64_t)dsc.slot * g.slot_bytes;
+  const SlotMeta sm = slot_meta(a.meta, g, dsc.slot);
+  const int n_o = dsc.n_o, n_q = dsc.n_q, t = dsc.t_next;
+  const bool accm = (t >= dsc.trig - g.W) && (t < dsc.trig);
+  const int tiles_o = (n_o + 1 + kTile - 1) / kTile;
+  const int tiles_q = (n_q + kTile - 1) / kTile;
+  const int S = a.n_splits, s = blockIdx.x;
+  const int o0 = (int)((int64_t)s * tiles_o / S), o1 = (int)((int64_t)(s + 1) * tiles_o / S);
+  const int q0 = (int)((int64_t)s * tiles_q / S), q1 = (int)((int64_t)(s + 1) * tiles_q / S);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tp = lane / LG, ld = lane % LG;
+  const int x0 = ld * 8;
+  const int row_stride = g.cap_o + g.cap_q;
+
+  const uint16_t* qp = a.q + ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * G) * d;
+  const uint16_t* kn = a.k + ((int64_t)(b * a.n_layers + li) * g.Hkv + kvh) * d;
+  const uint16_t* vn = a.v + ((int64_t)(b * a.n_layers + li) * g.Hkv + kvh) * d;
+  const float qs = g.sm_scale * kLog2e;
+
+  float qf[G][8];
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float f[8];
+    bf16x8_to_f(*(const uint4*)(qp + h * d + x0), f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qf[h][i] = f[i] * qs;
+  }
+  float m[G], l[G], o[G][8];
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    m[h] = -INFINITY;
+    l[h] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[h][i] = 0.f;
+  }
+
+  // Append the step's token (D1) — by the CTA owning the last Original tile.
+  if (o0 <= n_o / kTile && n_o / kTile < o1 && warp == 0) {
+    const int tt = n_o / kTile, j = n_o % kTile;
+    bool fits = (n_o + 1 <= g.cap_o) &&
+                ((int64_t)tiles_o * g.tile_o + (int64_t)tiles_q * g.tile_q <= g.slot_bytes);
+    if (!fits) {
+      if (lane == 0) atomicOr(a.err, kErrCapacity);
+    } else {
+      uint8_t* tb = o_tile_ptr(slot, g, tt);
+      for (int x = lane; x < d; x += 32) {
+        *(uint16_t*)(tb + o_k_off(g, j, x)) = kn[x];
+        *(uint16_t*)(tb + o_v_off(g, j, x)) = vn[x];
+      }
+      if (lane == 0) {
+        sm.pos_o[n_o] = t;
+        sm.acc_o[n_o] = make_float2(0.f, 0.f);
+      }
+    }
+  }
+
+  const int off = g.mode == ARKV_QUANT_SYM ? (1 << (g.bits - 1)) : 0;
+  const int n_work = (o1 - o0) + (q1 - q0);
+  for (int wi = warp; wi < n_work; wi += 4) {
+    const bool isq = wi >= (o1 - o0);
+    const int tile = isq ? q0 + (wi - (o1 - o0)) : o0 + wi;
+    const uint8_t* tb = isq ? q_tile_ptr(slot, g, tile) : o_tile_ptr(slot, g, tile);
+    for (int p0 = 0; p0 < kTile; p0 += TPP) {
+      const int j = p0 + tp;
+      const int row = tile * kTile + j;
+      const bool valid = isq ? row < n_q : row <= n_o;
+      float kf[8], vf[8];
+      if (valid) {
+        if (!isq) {
+          if (row == n_o) {
+            bf16x8_to_f(*(const uint4*)(kn + x0), kf);
+            bf16x8_to_f(*(const uint4*)(vn + x0), vf);
+          } else if (g.layout != ARKV_LAYOUT_FRAG) {
+            bf16x8_to_f(*(const uint4*)(tb + o_k_off(g, j, x0)), kf);
+            bf16x8_to_f(*(const uint4*)(tb + o_v_off(g, j, x0)), vf);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              kf[i] = bf16_to_f(*(const uint16_t*)(tb + o_k_off(g, j, x0 + i)));
+              vf[i] = bf16_to_f(*(const uint16_t*)(tb + o_v_off(g, j, x0 + i)));
+            }
+          }
+        } else {
+          const int grp = x0 / g.g;
+          const float ks = *(const float*)(tb + q_sc_off(g, j, 0, grp));
+          const float kz = *(const float*)(tb + q_sc_off(g, j, 1, grp));
+          const float vs = *(const float*)(tb + q_sc_off(g, j, 2, grp));
+          const float vz = *(const float*)(tb + q_sc_off(g, j, 3, grp));
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            int byte, shift;
+            q_k_loc(g, j, x0 + i, &byte, &shift);
+            int ck = (int)((tb[byte] >> shift) & ((1u << g.bits) - 1u)) - off;
+            q_v_loc(g, j, x0 + i, &byte, &shift);
+            int cv = (int)((tb[byte] >> shift) & ((1u << g.bits) - 1u)) - off;
+            kf[i] = (float)ck * ks + kz;
+            vf[i] = (float)cv * vs + vz;
+          }
+        }
+      }
+      float sc[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        float acc = 0.f;
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc = fmaf(qf[h][i], kf[i], acc);
+        }
+#pragma unroll
+        for (int msk = 1; msk < LG; msk <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, msk);
+        sc[h] = acc;
+      }
+      if (valid) {
+        if (accm && ld == 0) {
+          const int ridx = isq ? g.cap_o + row : row;
+#pragma unroll
+          for (int h = 0; h < G; ++h) a.logits[((int64_t)u * G + h) * row_stride + ridx] = sc[h];
+        }
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          float mn = fmaxf(m[h], sc[h]);
+          float cr = exp2f(m[h] - mn);
+          float p = exp2f(sc[h] - mn);
+          l[h] = l[h] * cr + p;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[h][i] = fmaf(p, vf[i], o[h][i] * cr);
+          m[h] = mn;
+        }
+      }
+    }
+  }
+
+  // merge the TPP lane groups of the warp (same dims, different tokens)
+#pragma unroll
+  for (int msk = LG; msk < 32; msk <<= 1) {
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      float mo = __shfl_xor_sync(0xffffffffu, m[h], msk);
+      float lo = __shfl_xor_sync(0xffffffffu, l[h], msk);
+      float mn = fmaxf(m[h], mo);
+      float ca = mn == -INFINITY ? 0.f : exp2f(m[h] - mn);
+      float cb = mn == -INFINITY ? 0.f : exp2f(mo - mn);
+      l[h] = l[h] * ca + lo * cb;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float oo = __shfl_xor_sync(0xffffffffu, o[h][i], msk);
+        o[h][i] = o[h][i] * ca + oo * cb;
+      }
+      m[h] = mn;
+    }
+  }
+  // merge the 4 warps through shared memory
+  __shared__ float sm_m[4][G], sm_l[4][G];
+  extern __shared__ float sm_o[];  // [4][G][d]
+  if (lane < LG) {
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      if (lane == 0) {
+        sm_m[warp][h] = m[h];
+        sm_l[warp][h] = l[h];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sm_o[(warp * G + h) * d + x0 + i] = o[h][i];
+    }
+  }
+  __syncthreads();
+  float* part = a.partials + ((int64_t)u * a.max_splits + s) * G * (d + 2);
+  for (int idx = threadIdx.x; idx < G * d; idx += blockDim.x) {
+    int h = idx / d, x = idx % d;
+    float M = -INFINITY;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w][h]);
+    float L = 0.f, O = 0.f;
+    for (int w = 0; w < 4; ++w) {
+      float c = (M == -INFINITY) ? 0.f : exp2f(sm_m[w][h] - M);
+      L += sm_l[w][h] * c;
+      O += sm_o[(w * G + h) * d + x] * c;
+    }
+    part[h * (d + 2) + 2 + x] = O;
+    if (x == 0) {
+      part[h * (d + 2) + 0] = M;
+      part[h * (d + 2) + 1] = L;
+    }
+  }
+}
+
+// Combine: merge split partials, write the output, HH accumulation, advance the unit.
+template <int G>
+__global__ void __launch_bounds__(256) decode_combine(DecodeArgs a) {
+  const Geom& g = a.g;
+  const int d = g.d;
+  int b, li, kvh, u;
+  unit_of(a, blockIdx.x, b, li, kvh, u);
+  const UnitDesc dsc = a.desc[u];
+  const int S = a.n_splits;
+  __shared__ float sM[G], sIL[G];
+  const float* part = a.partials + (int64_t)u * a.max_splits * G * (d + 2);
+  if (threadIdx.x < G) {
+    int h = threadIdx.x;
+    float M = -INFINITY;
+    for (int s = 0; s < S; ++s) M = fmaxf(M, part[(s * G + h) * (d + 2)]);
+    float L = 0.f;
+    for (int s = 0; s < S; ++s) {
+      float ms = part[(s * G + h) * (d + 2)];
+      if (ms != -INFINITY) L += part[(s * G + h) * (d + 2) + 1] * exp2f(ms - M);
+    }
+    sM[h] = M;
+    sIL[h] = 1.0f / L;
+  }
+  __syncthreads();
+  const int64_t obase = ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * G) * d;
+  for (int idx = threadIdx.x; idx < G * d; idx += blockDim.x) {
+    int h = idx / d, x = idx % d;
+    float O = 0.f;
+    for (int s = 0; s < S; ++s) {
+      float ms = part[(s * G + h) * (d + 2)];
+      if (ms != -INFINITY) O += part[(s * G + h) * (d + 2) + 2 + x] * exp2f(ms - sM[h]);
+    }
+    O *= sIL[h];
+    if (a.out_fp32)
+      ((float*)a.out)[obase + idx] = O;
+    else
+      ((uint16_t*)a.out)[obase + idx] = f_to_bf16_rne(O);
+  }
+  const int t = dsc.t_next;
+  const bool accm = (t >= dsc.trig - g.W) && (t < dsc.trig);
+  if (accm) {
+    const bool first = t == dsc.trig - g.W;
+    const SlotMeta sm = slot_meta(a.meta, g, dsc.slot);
+    const int row_stride = g.cap_o + g.cap_q;
+    const int n_rows = dsc.n_o + 1 + dsc.n_q;
+    for (int i = threadIdx.x; i < n_rows; i += blockDim.x) {
+      const bool isq = i > dsc.n_o;
+      const int ridx = isq ? g.cap_o + (i - dsc.n_o - 1) : i;
+      float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        float p = exp2f(a.logits[((int64_t)u * G + h) * row_stride + ridx] - sM[h]) * sIL[h];
+        a1 += p;
+        a2 += p * p;
+      }
+      float2* ap = isq ? &sm.acc_q[i - dsc.n_o - 1] : &sm.acc_o[i];
+      if (first) {
+        *ap = make_float2(a1, a2);
+      } else {
+        float2 c = *ap;
+        *ap = make_float2(c.x + a1, c.y + a2);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    UnitDesc nd = dsc;
+    nd.n_o = dsc.n_o + 1;
+    nd.t_next = dsc.t_next + 1;
+    a.desc[u] = nd;
+  }
+}
+
+// k_decode_fast.cu: returns -1 if the cache is not eligible.
+int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1);
+void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s);
+
+template <int G>
+static void launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+  dim3 grid(a.n_splits, n_units_call);
+  size_t smem = (size_t)4 * G * a.g.d * sizeof(float);
+  if (ev0) cudaEventRecord(ev0, s);
+  switch (a.g.d / 8) {
+#define LG_CASE(LGV) \
+  case LGV:          \
+    decode_split_generic<G, LGV><<<grid, 128, smem, s>>>(a); \
+    break;
+    LG_CASE(2)
+    LG_CASE(4)
+    LG_CASE(8)
+    LG_CASE(16)
+    LG_CASE(32)
+#undef LG_CASE
+    default:
+      break;
+  }
+  if (ev1) cudaEventRecord(ev1, s);
+  decode_combine<G><<<n_units_call, 256, 0, s>>>(a);
+}
+
+void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s) {
+  switch (a.g.G) {
+    case 1: decode_combine<1><<<n_units_call, 256, 0, s>>>(a); break;
+    case 2: decode_combine<2><<<n_units_call, 256, 0, s>>>(a); break;
+    case 4: decode_combine<4><<<n_units_call, 256, 0, s>>>(a); break;
+    case 8: decode_combine<8><<<n_units_call, 256, 0, s>>>(a); break;
+    default: break;
+  }
+}
+
+int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                  void* out, int out_fp32, uint8_t* slots, uint8_t* meta, UnitDesc* desc, float* partials,
+                  float* logits, int n_splits, int max_splits, int fast, int32_t* err, cudaStream_t s,
+                  cudaEvent_t ev0, cudaEvent_t ev1) {
+  DecodeArgs a;
+  a.g = g;
+  a.layer0 = layer0;
+  a.n_layers = n_layers;
+  a.n_splits = n_splits;
+  a.max_splits = max_splits;
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.slots = slots;
+  a.meta = meta;
+  a.desc = desc;
+  a.partials = partials;
+  a.logits = logits;
+  a.out = out;
+  a.out_fp32 = out_fp32;
+  a.err = err;
+  const int n_units_call = g.batch * n_layers * g.Hkv;
+  if (fast) return launch_decode_fast(a, n_units_call, s, ev0, ev1);
+  switch (g.G) {
+    case 1: launch_g<1>(a, n_units_call, s, ev0, ev1); break;
+    case 2: launch_g<2>(a, n_units_call, s, ev0, ev1); break;
+    case 4: launch_g<4>(a, n_units_call, s, ev0, ev1); break;
+    case 8: launch_g<8>(a, n_units_call, s, ev0, ev1); break;
+    default: return -1;
+  }
+  return 2;
+}
+
+}  // namespace arkv

@@ -1,0 +1,467 @@
+// k_tailor.cu — the tri-state tailor (D4-D6 / P4 of DESIGN.md §2).
+//
+//  select: heavy-hitter score S = μ + γ·max(0, acc2/N − μ²), μ = acc1/N, N = G·W
+//          (Eq. 9; R18, R20), then a block-wide 64-bit radix select of
+//          the two rank thresholds of Eq. 10 over composite keys
+//          (S desc, position asc; R22) -> new state per old row.
+//  scan:   block-wide exclusive scans -> for every NEW row its source row (the
+//          compaction map); writes the unit descriptor (counts, slot, next trigger).
+//  move:   one CTA per destination tile: gathers its 32 tokens (Original copy,
+//          Quantized -> Original promotion (R24), Original -> Quantized group
+//          quantization with fp32 scale/zero in the oracle's operation order (R23),
+//          Quantized -> Quantized code copy (R25)), assembles the tile in shared
+//          memory and writes it out with coalesced 16-byte stores into a fresh slot.
+#include "kernels.h"
+
+namespace arkv {
+
+enum : int32_t { kSrcInput = 1, kSrcOldO = 2, kSrcOldQ = 3 };
+
+__device__ __forceinline__ uint64_t hh_key(float2 acc, int pos, float invN, float gamma) {
+  float mu = __fmul_rn(acc.x, invN);
+  float var = __fsub_rn(__fmul_rn(acc.y, invN), __fmul_rn(mu, mu));
+  var = fmaxf(var, 0.f);
+  float S = __fadd_rn(mu, __fmul_rn(gamma, var));
+  uint32_t b = __float_as_uint(S);
+  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);  // order-preserving map of fp32
+  if (S == 0.f) b = 0x80000000u;                    // -0 == +0
+  return ((uint64_t)b << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)pos);
+}
+
+struct RowView {
+  const float2* acc_o;
+  const float2* acc_q;
+  const int32_t* pos_o;
+  const int32_t* pos_q;
+  int n_elig_o, n_q;
+  bool prefill;
+  __device__ void get(int i, float2& a, int& p) const {
+    if (i < n_elig_o) {
+      a = acc_o[i];
+      p = prefill ? i : pos_o[i];
+    } else {
+      a = acc_q[i - n_elig_o];
+      p = pos_q[i - n_elig_o];
+    }
+  }
+};
+
+__global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs jobs, uint8_t* meta,
+                                                             const float2* __restrict__ acc_pf,
+                                                             int8_t* __restrict__ st_scratch, int st_stride) {
+  __shared__ uint32_t hist[2][256];
+  __shared__ uint64_t sh_prefix[2];
+  __shared__ uint32_t sh_rem[2];
+  const TailorJob jb = jobs.j[blockIdx.x];
+  int8_t* st = st_scratch + (int64_t)blockIdx.x * st_stride;  // [old O rows | old Q rows]
+  const int n_elig_o = jb.n_o_old - jb.n_win_old;
+  const int n_e = n_elig_o + jb.n_q_old;
+  const int q_off = st_stride - g.cap_q;
+
+  // window rows are always Original (A13); identity jobs keep every row Original
+  for (int i = threadIdx.x; i < jb.n_o_old; i += blockDim.x)
+    if (i >= n_elig_o || jb.identity) st[i] = 1;
+  if (jb.identity) return;
+
+  RowView rv;
+  if (jb.old_slot < 0) {
+    rv.acc_o = acc_pf + (int64_t)jb.unit * g.max_pos;
+    rv.pos_o = nullptr;
+    rv.acc_q = nullptr;
+    rv.pos_q = nullptr;
+    rv.prefill = true;
+  } else {
+    SlotMeta sm = slot_meta(meta, g, jb.old_slot);
+    rv.acc_o = sm.acc_o;
+    rv.acc_q = sm.acc_q;
+    rv.pos_o = sm.pos_o;
+    rv.pos_q = sm.pos_q;
+    rv.prefill = false;
+  }
+  rv.n_elig_o = n_elig_o;
+  rv.n_q = jb.n_q_old;
+  const float invN = 1.0f / (float)(g.G * g.W);
+  const float gamma = g.gamma;
+
+  const uint32_t kk[2] = {(uint32_t)jb.n_oe, (uint32_t)(jb.n_oe + jb.n_q_new)};
+  if (threadIdx.x < 2) {
+    sh_prefix[threadIdx.x] = 0;
+    sh_rem[threadIdx.x] = kk[threadIdx.x];
+  }
+  uint64_t mask = 0;
+  for (int pass = 7; pass >= 0; --pass) {
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) (&hist[0][0])[i] = 0;
+    __syncthreads();
+    const uint64_t p0 = sh_prefix[0], p1 = sh_prefix[1];
+    const int sh = pass * 8;
+    for (int i = threadIdx.x; i < n_e; i += blockDim.x) {
+      float2 a;
+      int p;
+      rv.get(i, a, p);
+      uint64_t key = hh_key(a, p, invN, gamma);
+      uint32_t dg = (uint32_t)(key >> sh) & 0xFFu;
+      if ((key & mask) == p0) atomicAdd(&hist[0][dg], 1u);
+      if ((key & mask) == p1) atomicAdd(&hist[1][dg], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      int s = threadIdx.x;
+      uint32_t rem = sh_rem[s];
+      if (rem > 0) {
+        uint32_t cum = 0;
+        for (int dgt = 255; dgt >= 0; --dgt) {
+          uint32_t h = hist[s][dgt];
+          if (cum + h >= rem) {
+            sh_prefix[s] |= ((uint64_t)dgt) << sh;
+            sh_rem[s] = rem - cum;
+            break;
+          }
+          cum += h;
+        }
+      }
+    }
+    mask |= 0xFFull << sh;
+    __syncthreads();
+  }
+  // thresholds: k-th largest key (k == 0 -> nothing selected)
+  const uint64_t T1 = kk[0] == 0 ? ~0ull : sh_prefix[0];
+  const uint64_t T2 = kk[1] == 0 ? ~0ull : sh_prefix[1];
+  for (int i = threadIdx.x; i < n_e; i += blockDim.x) {
+    float2 a;
+    int p;
+    rv.get(i, a, p);
+    uint64_t key = hh_key(a, p, invN, gamma);
+    int8_t s = key >= T1 ? 1 : (key >= T2 ? 2 : 3);
+    if (i < n_elig_o)
+      st[i] = s;
+    else
+      st[q_off + (i - n_elig_o)] = s;
+  }
+}
+
+// Block-wide exclusive scan of two counters.
+__device__ int2 block_exscan2(int2 v, int2* sh, int2* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int2 x = v;
+  for (int off = 1; off < 32; off <<= 1) {
+    int a = __shfl_up_sync(0xffffffffu, x.x, off);
+    int b = __shfl_up_sync(0xffffffffu, x.y, off);
+    if (lane >= off) {
+      x.x += a;
+      x.y += b;
+    }
+  }
+  __syncthreads();
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int2 run = make_int2(0, 0);
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      int2 t = sh[i];
+      sh[i] = run;
+      run.x += t.x;
+      run.y += t.y;
+    }
+    sh[32] = run;
+  }
+  __syncthreads();
+  int2 base = sh[w];
+  *total = sh[32];
+  return make_int2(base.x + x.x - v.x, base.y + x.y - v.y);
+}
+
+__global__ void __launch_bounds__(1024) tailor_scan_kernel(Geom g, TailorJobs jobs, UnitDesc* desc,
+                                                           const int8_t* __restrict__ st_scratch, int st_stride,
+                                                           int32_t* __restrict__ src_scratch, int src_stride,
+                                                           int32_t* err) {
+  __shared__ int2 sh[33];
+  const TailorJob jb = jobs.j[blockIdx.x];
+  const int8_t* st = st_scratch + (int64_t)blockIdx.x * st_stride;
+  const int q_off = st_stride - g.cap_q;
+  int32_t* src_o = src_scratch + (int64_t)blockIdx.x * src_stride;
+  int32_t* src_q = src_o + g.cap_o;
+  const int n_elig_o = jb.n_o_old - jb.n_win_old;
+  const int kindO = jb.old_slot < 0 ? kSrcInput : kSrcOldO;
+
+  // S1: old eligible O rows; S2: old Q rows.
+  int2 tot1, tot2;
+  {
+    const int n = n_elig_o;
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int a = threadIdx.x * per, b = min(a + per, n);
+    int2 c = make_int2(0, 0);
+    for (int i = a; i < b; ++i) {
+      c.x += st[i] == 1;
+      c.y += st[i] == 2;
+    }
+    int2 ex = block_exscan2(c, sh, &tot1);
+    // placed after the S2 counts are known: compute S2 totals first
+    __syncthreads();
+    const int n2 = jb.n_q_old;
+    const int per2 = (n2 + blockDim.x - 1) / blockDim.x;
+    const int a2 = threadIdx.x * per2, b2 = min(a2 + per2, n2);
+    int2 c2 = make_int2(0, 0);
+    for (int i = a2; i < b2; ++i) {
+      c2.x += st[q_off + i] == 1;
+      c2.y += st[q_off + i] == 2;
+    }
+    int2 ex2 = block_exscan2(c2, sh, &tot2);
+    // S1 rows: O -> new O index ex.x + ...; Q -> new Q index tot2.y + ex.y + ...
+    int o = ex.x, q = tot2.y + ex.y;
+    for (int i = a; i < b; ++i) {
+      int8_t s = st[i];
+      if (s == 1) src_o[o++] = (kindO << 28) | i;
+      else if (s == 2) src_q[q++] = (kindO << 28) | i;
+    }
+    // S2 rows: O -> tot1.x + ex2.x + ...; Q -> ex2.y + ...
+    int o2 = tot1.x + ex2.x, q2 = ex2.y;
+    for (int i = a2; i < b2; ++i) {
+      int8_t s = st[q_off + i];
+      if (s == 1) src_o[o2++] = (kSrcOldQ << 28) | i;
+      else if (s == 2) src_q[q2++] = (kSrcOldQ << 28) | i;
+    }
+  }
+  // window rows (old O rows [n_elig_o, n_o_old)) close the new O segment in order
+  const int n_oe_got = tot1.x + tot2.x;
+  for (int i = threadIdx.x; i < jb.n_win_old; i += blockDim.x)
+    src_o[n_oe_got + i] = (kindO << 28) | (n_elig_o + i);
+  if (threadIdx.x == 0) {
+    const int n_q_got = tot1.y + tot2.y;
+    if (n_oe_got != jb.n_oe || n_q_got != jb.n_q_new) atomicOr(err, kErrIntegrity);
+    UnitDesc dd;
+    dd.slot = jb.new_slot;
+    dd.n_o = jb.n_oe + jb.n_win_old;
+    dd.n_q = jb.n_q_new;
+    dd.t_next = jb.t_next;
+    dd.trig = jb.trig_new;
+    dd.pad0 = dd.pad1 = dd.pad2 = 0;
+    desc[jb.unit] = dd;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Move: build destination tiles.
+// ---------------------------------------------------------------------------------
+struct SrcRef {
+  const uint8_t* old_slot;
+  const uint16_t* pk;  // prefill rows of this unit [P][d]
+  const uint16_t* pv;
+};
+
+__device__ __forceinline__ uint32_t read_code(const Geom& g, const uint8_t* tile, int j, int x, bool isv) {
+  int byte, shift;
+  if (isv) q_v_loc(g, j, x, &byte, &shift);
+  else q_k_loc(g, j, x, &byte, &shift);
+  uint32_t w = tile[byte];
+  if (g.bits == 8) return w;
+  return (w >> shift) & ((1u << g.bits) - 1u);
+}
+
+__device__ __forceinline__ void write_code(const Geom& g, uint8_t* tile, int j, int x, bool isv, uint32_t c) {
+  int byte, shift;
+  if (isv) q_v_loc(g, j, x, &byte, &shift);
+  else q_k_loc(g, j, x, &byte, &shift);
+  // codes of different dims/tokens may share a 32-bit word: OR into the zeroed tile
+  uint32_t* wp = (uint32_t*)(tile + (byte & ~3));
+  atomicOr(wp, c << (shift + 8 * (byte & 3)));
+}
+
+__device__ __forceinline__ float read_o(const Geom& g, const uint8_t* tile, int j, int x, bool isv) {
+  int off = isv ? o_v_off(g, j, x) : o_k_off(g, j, x);
+  return bf16_to_f(*(const uint16_t*)(tile + off));
+}
+
+template <int VPL>  // values per lane = ceil(d / 32)
+__global__ void __launch_bounds__(256) tailor_move_kernel(Geom g, TailorJobs jobs, uint8_t* slots, uint8_t* meta,
+                                                          const uint16_t* __restrict__ pk,
+                                                          const uint16_t* __restrict__ pv, int P,
+                                                          const int32_t* __restrict__ src_scratch, int src_stride) {
+  extern __shared__ __align__(16) uint8_t tile[];
+  const TailorJob jb = jobs.j[blockIdx.y];
+  const int n_o_new = jb.n_oe + jb.n_win_old;
+  const int tiles_o = (n_o_new + kTile - 1) / kTile;
+  const int tiles_q = (jb.n_q_new + kTile - 1) / kTile;
+  int tid = blockIdx.x;
+  if (tid >= tiles_o + tiles_q) return;
+  const bool dstQ = tid >= tiles_o;
+  if (dstQ) tid -= tiles_o;
+  const int tbytes = dstQ ? g.tile_q : g.tile_o;
+  for (int i = threadIdx.x * 4; i < tbytes; i += blockDim.x * 4) *(uint32_t*)(tile + i) = 0u;
+  __syncthreads();
+
+  const int32_t* src = src_scratch + (int64_t)blockIdx.y * src_stride + (dstQ ? g.cap_o : 0);
+  uint8_t* nslot = slots + (int64_t)jb.new_slot * g.slot_bytes;
+  const uint8_t* oslot = jb.old_slot >= 0 ? slots + (int64_t)jb.old_slot * g.slot_bytes : nullptr;
+  SlotMeta nm = slot_meta(meta, g, jb.new_slot);
+  SlotMeta om;
+  if (jb.old_slot >= 0) om = slot_meta(meta, g, jb.old_slot);
+  const uint16_t* upk = pk ? pk + (int64_t)jb.unit * P * g.d : nullptr;
+  const uint16_t* upv = pv ? pv + (int64_t)jb.unit * P * g.d : nullptr;
+  const int n_new = dstQ ? jb.n_q_new : n_o_new;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qmaxv = (1 << (g.bits - 1)) - 1;
+  const int off = g.mode == ARKV_QUANT_SYM ? (1 << (g.bits - 1)) : 0;
+
+  for (int j = warp; j < kTile; j += blockDim.x >> 5) {
+    const int row = tid * kTile + j;
+    if (row >= n_new) continue;
+    const int32_t sref = src[row];
+    const int kind = sref >> 28, orow = sref & 0x0FFFFFFF;
+    int pos;
+    if (kind == kSrcInput) pos = orow;
+    else if (kind == kSrcOldO) pos = om.pos_o[orow];
+    else pos = om.pos_q[orow];
+    if (lane == 0) {
+      if (dstQ) {
+        nm.pos_q[row] = pos;
+        nm.acc_q[row] = make_float2(0.f, 0.f);
+      } else {
+        nm.pos_o[row] = pos;
+        nm.acc_o[row] = make_float2(0.f, 0.f);
+      }
+    }
+    const uint8_t* qt = nullptr;
+    const uint8_t* ot = nullptr;
+    int oj = orow & 31;
+    if (kind == kSrcOldQ) qt = q_tile_ptr((uint8_t*)oslot, g, orow >> 5);
+    if (kind == kSrcOldO) ot = o_tile_ptr((uint8_t*)oslot, g, orow >> 5);
+
+    if (kind == kSrcOldQ && dstQ) {
+      // Q -> Q: copy codes and scales (R25)
+      for (int x = lane; x < g.d; x += 32) {
+        write_code(g, tile, j, x, false, read_code(g, qt, oj, x, false));
+        write_code(g, tile, j, x, true, read_code(g, qt, oj, x, true));
+      }
+      for (int w = lane; w < 4 * g.ng; w += 32) {
+        int which = w / g.ng, grp = w % g.ng;
+        *(float*)(tile + q_sc_off(g, j, which, grp)) = *(const float*)(qt + q_sc_off(g, oj, which, grp));
+      }
+      continue;
+    }
+    // materialise bf16 values (K and V) for this token
+    float kvv[2][VPL];
+#pragma unroll
+    for (int t = 0; t < VPL; ++t) {
+      int x = lane + 32 * t;
+      float kx = 0.f, vx = 0.f;
+      if (x < g.d) {
+        if (kind == kSrcInput) {
+          kx = bf16_to_f(upk[(int64_t)orow * g.d + x]);
+          vx = bf16_to_f(upv[(int64_t)orow * g.d + x]);
+        } else if (kind == kSrcOldO) {
+          kx = read_o(g, ot, oj, x, false);
+          vx = read_o(g, ot, oj, x, true);
+        } else {
+          // Q -> O promotion (R24): bf16_rne(f32(f32(code*s) + z))
+          int grp = x / g.g;
+          float ks = *(const float*)(qt + q_sc_off(g, oj, 0, grp));
+          float kz = *(const float*)(qt + q_sc_off(g, oj, 1, grp));
+          float vs = *(const float*)(qt + q_sc_off(g, oj, 2, grp));
+          float vz = *(const float*)(qt + q_sc_off(g, oj, 3, grp));
+          int ck = (int)read_code(g, qt, oj, x, false) - off;
+          int cv = (int)read_code(g, qt, oj, x, true) - off;
+          kx = bf16_to_f(f_to_bf16_rne(__fadd_rn(__fmul_rn((float)ck, ks), kz)));
+          vx = bf16_to_f(f_to_bf16_rne(__fadd_rn(__fmul_rn((float)cv, vs), vz)));
+        }
+      }
+      kvv[0][t] = kx;
+      kvv[1][t] = vx;
+    }
+    if (!dstQ) {
+#pragma unroll
+      for (int t = 0; t < VPL; ++t) {
+        int x = lane + 32 * t;
+        if (x < g.d) {
+          *(uint16_t*)(tile + o_k_off(g, j, x)) = (uint16_t)(__float_as_uint(kvv[0][t]) >> 16);
+          *(uint16_t*)(tile + o_v_off(g, j, x)) = (uint16_t)(__float_as_uint(kvv[1][t]) >> 16);
+        }
+      }
+      continue;
+    }
+    // O -> Q: group quantization (R23), fp32 op order identical to the oracle
+    for (int kv = 0; kv < 2; ++kv) {
+      for (int grp = 0; grp < g.ng; ++grp) {
+        float mn = INFINITY, mx = -INFINITY, am = 0.f;
+#pragma unroll
+        for (int t = 0; t < VPL; ++t) {
+          int x = lane + 32 * t;
+          if (x < g.d && x / g.g == grp) {
+            float v = kvv[kv][t];
+            mn = fminf(mn, v);
+            mx = fmaxf(mx, v);
+            am = fmaxf(am, fabsf(v));
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+        }
+        float s, z;
+        bool flat;
+        if (g.mode == ARKV_QUANT_SYM) {
+          flat = am == 0.f;
+          s = flat ? 1.f : __fdiv_rn(am, (float)qmaxv);
+          z = 0.f;
+        } else {
+          flat = mx == mn;
+          s = flat ? 1.f : __fdiv_rn(__fsub_rn(mx, mn), (float)((1 << g.bits) - 1));
+          z = mn;
+        }
+#pragma unroll
+        for (int t = 0; t < VPL; ++t) {
+          int x = lane + 32 * t;
+          if (x < g.d && x / g.g == grp) {
+            int c;
+            if (flat) {
+              c = 0;
+            } else if (g.mode == ARKV_QUANT_SYM) {
+              c = __float2int_rn(__fdiv_rn(kvv[kv][t], s));
+              c = max(-qmaxv, min(qmaxv, c));
+            } else {
+              c = __float2int_rn(__fdiv_rn(__fsub_rn(kvv[kv][t], mn), s));
+              c = max(0, min((1 << g.bits) - 1, c));
+            }
+            write_code(g, tile, j, x, kv == 1, (uint32_t)(c + off));
+          }
+        }
+        if (lane == 0) {
+          *(float*)(tile + q_sc_off(g, j, kv * 2 + 0, grp)) = s;
+          *(float*)(tile + q_sc_off(g, j, kv * 2 + 1, grp)) = z;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  uint8_t* dst = dstQ ? q_tile_ptr(nslot, g, tid) : o_tile_ptr(nslot, g, tid);
+  for (int i = threadIdx.x * 16; i < tbytes; i += blockDim.x * 16) *(uint4*)(dst + i) = *(const uint4*)(tile + i);
+}
+
+int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_tiles, uint8_t* slots, uint8_t* meta,
+                  UnitDesc* desc, const uint16_t* pk, const uint16_t* pv, int P, const float2* acc_pf,
+                  int8_t* st_scratch, int32_t* src_scratch, int32_t* err, cudaStream_t s) {
+  const int st_stride = max(g.max_pos, g.cap_o) + g.cap_q;
+  const int src_stride = g.cap_o + g.cap_q;
+  tailor_select_kernel<<<n_jobs, 1024, 0, s>>>(g, jobs, meta, acc_pf, st_scratch, st_stride);
+  tailor_scan_kernel<<<n_jobs, 1024, 0, s>>>(g, jobs, desc, st_scratch, st_stride, src_scratch, src_stride, err);
+  size_t smem = (size_t)max(g.tile_o, g.tile_q);
+  dim3 grid(max_tiles, n_jobs);
+  const int vpl = (g.d + 31) / 32;
+#define MV_CASE(V)                                                                                                \
+  case V:                                                                                                         \
+    cudaFuncSetAttribute(tailor_move_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
+    tailor_move_kernel<V><<<grid, 256, smem, s>>>(g, jobs, slots, meta, pk, pv, P, src_scratch, src_stride);      \
+    break;
+  switch (vpl) {
+    MV_CASE(1)
+    MV_CASE(2)
+    MV_CASE(4)
+    MV_CASE(8)
+    default:
+      return -1;
+  }
+#undef MV_CASE
+  return 3;
+}
+
+}  // namespace arkv

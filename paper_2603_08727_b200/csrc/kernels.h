@@ -1,0 +1,65 @@
+// kernels.h — host-side launch wrappers of the ARKV device kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace arkv {
+
+constexpr int kMaxJobs = 96;  // tailor jobs per launch (kernel-parameter array)
+
+// One unit's tailor (Eq. 10) in a wave: sources -> a fresh slot.
+struct TailorJob {
+  int32_t unit;       // global unit index (b*L + l)*H_kv + kvh
+  int32_t old_slot;   // -1 for the prefill tailor (sources are the prompt rows)
+  int32_t new_slot;
+  int32_t n_o_old;    // old Original rows (prefill: P)
+  int32_t n_q_old;    // old Quantized rows (prefill: 0)
+  int32_t n_win_old;  // window rows present in the old rows (prefill W, decode W-1)
+  int32_t n_oe;       // eligible tokens kept Original
+  int32_t n_q_new;    // tokens kept Quantized
+  int32_t trig_new;   // next tailor position
+  int32_t t_next;     // position of the next appended token
+  int32_t identity;   // 1: no selection, every old row stays Original (prefill ingest)
+  int32_t pad;
+};
+struct TailorJobs {
+  TailorJob j[kMaxJobs];
+};
+
+// Prefill statistics: passes 1-2 + local Eq. 3 column sums; then the
+// moments / OQ score from (possibly all-reduced) column sums.  Return launches.
+int launch_prefill_begin(const Geom& g, const uint16_t* q_win, const uint16_t* k, int P, float* partials,
+                         int n_chunks1, float2* acc_pf, double* colsum, cudaStream_t s);
+int launch_prefill_finish(const Geom& g, const double* colsum, int P, double* stats, double* oq, const double* tau,
+                          double stat_eps, cudaStream_t s);
+
+// Tailor of a wave of jobs (D4-D6).
+int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_tiles, uint8_t* slots, uint8_t* meta,
+                  UnitDesc* desc, const uint16_t* pk, const uint16_t* pv, int P, const float2* acc_pf,
+                  int8_t* st_scratch, int32_t* src_scratch, int32_t* err, cudaStream_t s);
+
+struct DecodeArgs {
+  Geom g;
+  int layer0, n_layers, n_splits, max_splits;
+  const uint16_t* q;
+  const uint16_t* k;
+  const uint16_t* v;
+  uint8_t* slots;
+  uint8_t* meta;
+  UnitDesc* desc;
+  float* partials;
+  float* logits;
+  void* out;
+  int out_fp32;
+  int32_t* err;
+};
+
+// Decode attention (D1, D3, D7) for units [layer0, layer0+n) of all sequences.
+int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                  void* out, int out_fp32, uint8_t* slots, uint8_t* meta, UnitDesc* desc, float* partials,
+                  float* logits, int n_splits, int max_splits, int fast, int32_t* err, cudaStream_t s,
+                  cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+
+}  // namespace arkv

@@ -1,0 +1,101 @@
+"""CPU-only checks of the C ABI: the library builds/loads without a GPU, exports every
+symbol include/arkv.h declares, and its host logic (count schedule, OQ score) equals
+the oracle's independent implementation."""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+import oracle as O
+from paper_2603_08727_b200 import arkv as A
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2603_08727_b200.build import build
+    build()
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "arkv.h")).read()
+    declared = set(re.findall(r"\b(arkv_[a-z_]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    L = A.lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    assert set(A.EXPORTED) <= declared
+
+
+def test_version_and_status_strings():
+    assert "sm_100a" in A.arkv_version()
+    assert A.lib().arkv_status_string(-4).decode().startswith("prompt shorter")
+
+
+def test_config_validation():
+    c = A.make_config(1, 4, 3, 16)          # H_q % H_kv != 0
+    with pytest.raises(A.ArkvError):
+        A.arkv_cache_bytes(c)
+    c = A.make_config(1, 4, 2, 16, window=8, budget_tokens=16)   # B <= 2W (R14)
+    with pytest.raises(A.ArkvError):
+        A.arkv_cache_bytes(c)
+    c = A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, quant_bits=3)
+    with pytest.raises(A.ArkvError):
+        A.arkv_cache_bytes(c)
+    c = A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, layout=A.LAYOUT_FRAG)  # d % 32 != 0
+    with pytest.raises(A.ArkvError):
+        A.arkv_cache_bytes(c)
+    a, w = A.arkv_cache_bytes(A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, max_positions=128))
+    assert a > 0 and w > 0
+
+
+def test_arena_respects_budget():
+    """The persistent arena is ~B_bytes per unit (+ tile slack and metadata), i.e. the
+    4x reduction of configs[1] is physical: arena < dense bf16 / 3."""
+    c = A.make_config(32, 32, 8, 128, budget_tokens=8192, max_positions=32768 + 4096, max_prompt=32768)
+    arena, _ = A.arkv_cache_bytes(c)
+    dense = 32 * 8 * (32768 + 4096) * 512
+    assert arena < dense / 3
+
+
+def _ocfg(c: A.ArkvConfig) -> O.Cfg:
+    return O.Cfg(n_layers=c.n_layers, n_q_heads=c.n_q_heads, n_kv_heads=c.n_kv_heads, head_dim=c.head_dim,
+                 window=c.window, budget_tokens=c.budget_tokens, quant_bits=c.quant_bits,
+                 group_size=c.group_size or c.head_dim, alpha=c.alpha)
+
+
+def test_schedule_appendix_config2():
+    c = A.make_config(32, 32, 8, 128, budget_tokens=8192, max_positions=40000, max_prompt=32768)
+    for rho in (1.0, 0.5, 0.3):
+        assert A.arkv_schedule(c, 32768, rho, 4096) == O.schedule(32768, 4096, rho, _ocfg(c))
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.integers(4, 3000), st.integers(0, 1500), st.floats(0.01, 1.0), st.integers(1, 48),
+       st.sampled_from([(16, 4, 16), (128, 4, 128), (128, 4, 32), (64, 2, 64), (128, 8, 64), (32, 8, 8)]))
+def test_host_schedule_equals_oracle(P, steps, rho, W, dbg):
+    d, bits, g = dbg
+    B = 2 * W + 1 + (P // 3)
+    c = A.make_config(1, 1, 1, d, window=W, budget_tokens=B, quant_bits=bits, group_size=g,
+                      max_positions=P + steps + 1, max_prompt=P)
+    assert A.arkv_schedule(c, P, rho, steps) == O.schedule(P, steps, rho, _ocfg(c))
+
+
+@pytest.mark.parametrize("p", [[0.25] * 4, [1, 0, 0, 0], [0.5, 0.25, 0.125, 0.125], [0.1, 0.2, 0.3, 0.4]])
+def test_host_oq_score_equals_oracle(p):
+    p = np.array(p, dtype=float)
+    n = len(p)
+    nz = p > 0
+    H = float(-(p[nz] * np.log(p[nz])).sum())
+    m2 = float(((p - 1 / n) ** 2).sum() / n)
+    m4 = float(((p - 1 / n) ** 4).sum() / n)
+    c = A.make_config(1, 1, 1, 16, window=1, budget_tokens=8)
+    stats, score = A.arkv_oq_score(c, H, m2, m4)
+    ref = O.compute_stats(p)
+    np.testing.assert_allclose(stats, ref, rtol=1e-12)
+    assert score == pytest.approx(O.oq_score(*ref), rel=1e-12)

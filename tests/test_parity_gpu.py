@@ -1,0 +1,209 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on the same
+seeded inputs.
+
+Bars (BASELINE.json north_star): token states, quantization codes, fp32 scales/zeros
+and Original bf16 values bit-exact; attention outputs within 2e-3 relative / 1e-3
+absolute; per-layer statistics within 1e-4 relative.  Decode inputs use the
+"margin" recipe so fp32 (GPU) and fp64 (oracle) heavy-hitter rankings agree; the
+oracle asserts the margin at both rank thresholds of every tailor.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import Shape, prefill_inputs, decode_inputs
+
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 2e-3, 1e-3
+STAT_RTOL = 1e-4
+# Heavy-hitter scores are sums of <= G*W = 128 fp32 terms on the GPU (relative error
+# < 1e-6); a relative gap of 1e-5 at each rank threshold makes fp32 and fp64 rank alike.
+MARGIN = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda_and_lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2603_08727_b200.build import build
+    build()
+
+
+def _np(t):
+    return t.double().cpu().numpy()
+
+
+def _bf16_bits_to_f64(u16):
+    return (u16.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def make_pair(sh: Shape, budget, bits=4, g=0, mode="asym", layout=0, steps=64, decode_kernel=0, max_splits=0,
+              n_spare=0):
+    from paper_2603_08727_b200 import arkv as A
+    cfg = A.make_config(sh.n_layers, sh.n_q_heads, sh.n_kv_heads, sh.head_dim, batch=sh.batch, window=sh.window,
+                        budget_tokens=budget, quant_bits=bits, group_size=g,
+                        quant_mode=A.QUANT_SYM if mode == "sym" else A.QUANT_ASYM,
+                        max_positions=sh.prompt_len + steps + 1, max_prompt=sh.prompt_len, layout=layout,
+                        decode_kernel=decode_kernel, max_splits=max_splits, n_spare_slots=n_spare)
+    gpu = A.ArkvCache(cfg, "cuda")
+    ocfg = O.Cfg(n_layers=sh.n_layers, n_q_heads=sh.n_q_heads, n_kv_heads=sh.n_kv_heads, head_dim=sh.head_dim,
+                 batch=sh.batch, window=sh.window, budget_tokens=budget, quant_bits=bits, group_size=g or sh.head_dim,
+                 quant_mode=mode)
+    return gpu, O.OracleARKV(ocfg), ocfg
+
+
+def compare_unit(gpu, ora, b, l, kvh, where=""):
+    e = gpu.arkv_export_unit(b, l, kvh)
+    r = ora.export(b, l, kvh)
+    tag = f"{where} unit ({b},{l},{kvh})"
+    np.testing.assert_array_equal(e["state"], r["state"], err_msg="states " + tag)
+    assert e["n_o"] == r["n_o"] and e["n_q"] == r["n_q"], tag
+    o = r["state"] == 1
+    np.testing.assert_array_equal(_bf16_bits_to_f64(e["o_k"])[o], r["o_k"][o], err_msg="O keys " + tag)
+    np.testing.assert_array_equal(_bf16_bits_to_f64(e["o_v"])[o], r["o_v"][o], err_msg="O values " + tag)
+    q = r["state"] == 2
+    np.testing.assert_array_equal(e["q_k"][q], r["q_k"][q], err_msg="K codes " + tag)
+    np.testing.assert_array_equal(e["q_v"][q], r["q_v"][q], err_msg="V codes " + tag)
+    for key in ("k_scale", "k_zero", "v_scale", "v_zero"):
+        np.testing.assert_array_equal(e[key][q], r[key][q], err_msg=key + " " + tag)
+
+
+def run_parity(sh: Shape, budget, steps, seed=0, recipe="margin", rho=None, check_every=1, **kw):
+    gpu, ora, ocfg = make_pair(sh, budget, steps=steps, **kw)
+    qw, k, v = prefill_inputs(sh, seed=seed, recipe=recipe)
+    stats, oq, rho_gpu = gpu.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda(), rho_override=rho)
+    ora.prefill(_np(qw), _np(k), _np(v), rho_override=rho_gpu)
+    gpu.arkv_check()
+    for b in range(sh.batch):
+        for l in range(sh.n_layers):
+            for h in range(sh.n_kv_heads):
+                compare_unit(gpu, ora, b, l, h, "after prefill")
+    worst = 0.0
+    for s in range(steps):
+        q, kn, vn = decode_inputs(sh, s, seed=seed, recipe=recipe)
+        out = gpu.arkv_decode_step(q.cuda(), kn.cuda(), vn.cuda(), out_fp32=True)
+        ref = ora.decode_step(_np(q), _np(kn), _np(vn))
+        got = out.double().cpu().numpy()
+        np.testing.assert_allclose(got, ref, rtol=RTOL, atol=ATOL, err_msg=f"output step {s}")
+        worst = max(worst, float(np.max(np.abs(got - ref) / (ATOL + RTOL * np.abs(ref)))))
+        if (s + 1) % check_every == 0 or s == steps - 1:
+            gpu.arkv_check()
+            for b in range(sh.batch):
+                for l in range(sh.n_layers):
+                    for h in range(sh.n_kv_heads):
+                        compare_unit(gpu, ora, b, l, h, f"step {s}")
+    margins = [m for u in ora.units.values() for m in u.margins]
+    n_tailors = sum(len(u.tailors) for u in ora.units.values())
+    if margins:
+        assert min(margins) > MARGIN, f"test input lacks a score margin ({min(margins):.2e})"
+    return dict(worst=worst, tailors=n_tailors, stats=stats.cpu().numpy(), oq=oq.cpu().numpy(), rho=rho_gpu,
+                gpu=gpu, ora=ora)
+
+
+TOY = Shape(batch=1, n_layers=1, n_q_heads=4, n_kv_heads=2, head_dim=16, prompt_len=64, window=8)
+
+
+@pytest.mark.parametrize("rho", [1.0, 0.5, 0.25])
+def test_toy_config(rho):
+    """BASELINE configs[0] (R29: W = 8, injected rho): 64-token prefill + 16 steps."""
+    r = run_parity(TOY, budget=32, steps=16, seed=11, rho=[[rho]], bits=4, g=16)
+    assert r["tailors"] >= 2
+
+
+def test_toy_two_layers_stats_rho():
+    sh = Shape(batch=1, n_layers=2, n_q_heads=4, n_kv_heads=2, head_dim=16, prompt_len=64, window=8)
+    run_parity(sh, budget=32, steps=24, seed=3, bits=4, g=16)
+
+
+MID = Shape(batch=1, n_layers=2, n_q_heads=8, n_kv_heads=2, head_dim=128, prompt_len=2048, window=32)
+
+
+@pytest.mark.parametrize("layout,bits,g,mode", [
+    (2, 4, 128, "asym"),   # FRAG, paper default
+    (2, 4, 32, "asym"),
+    (1, 4, 128, "asym"),   # PLAIN
+    (1, 2, 32, "asym"),
+    (1, 8, 128, "sym"),
+    (2, 4, 64, "sym"),
+])
+def test_mid_config(layout, bits, g, mode):
+    """L=2, H_q=8, H_kv=2, d=128, P=2048, B=512: prefill tailor + decode tailors."""
+    r = run_parity(MID, budget=512, steps=80, seed=5, rho=[[1.0, 0.4]], layout=layout, bits=bits, g=g, mode=mode,
+                   check_every=20)
+    assert r["tailors"] >= 2 * 2 * 2
+
+
+def test_generic_kernel_on_frag_layout():
+    run_parity(MID, budget=512, steps=40, seed=6, rho=[[0.7, 0.3]], layout=2, decode_kernel=1, check_every=40)
+
+
+def test_batch_and_spare_waves():
+    """Batch 3 with only 2 staging slots: every tailor runs in several waves."""
+    sh = Shape(batch=3, n_layers=2, n_q_heads=4, n_kv_heads=2, head_dim=32, prompt_len=200, window=8)
+    run_parity(sh, budget=64, steps=40, seed=9, rho=[[1.0, 0.5], [0.3, 1.0], [0.6, 0.6]], layout=2, bits=4, g=32,
+               n_spare=2, check_every=10)
+
+
+def test_no_prefill_tailor_path():
+    """P <= B - W: the prompt is ingested as Original; the first tailor happens in decode."""
+    sh = Shape(batch=1, n_layers=1, n_q_heads=4, n_kv_heads=1, head_dim=32, prompt_len=40, window=8)
+    r = run_parity(sh, budget=64, steps=40, seed=2, rho=[[0.5]], bits=4, g=32)
+    assert r["tailors"] >= 1
+
+
+def test_short_prompt_requires_override():
+    from paper_2603_08727_b200 import arkv as A
+    sh = Shape(batch=1, n_layers=1, n_q_heads=2, n_kv_heads=1, head_dim=16, prompt_len=5, window=8)
+    gpu, ora, _ = make_pair(sh, budget=32, steps=8)
+    qw, k, v = prefill_inputs(sh, seed=1)
+    with pytest.raises(A.ArkvError):
+        gpu.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda())
+    run_parity(sh, budget=32, steps=8, seed=1, rho=[[1.0]])
+
+
+def test_prefill_statistics_natural():
+    """Eqs. 3-7 on natural-recipe inputs: H, V, K and q within 1e-4 relative; rho too."""
+    sh = Shape(batch=2, n_layers=3, n_q_heads=8, n_kv_heads=2, head_dim=128, prompt_len=3000, window=32)
+    from paper_2603_08727_b200 import arkv as A
+    cfg = A.make_config(3, 8, 2, 128, batch=2, budget_tokens=512, max_positions=3100, max_prompt=3000)
+    gpu = A.ArkvCache(cfg)
+    qw, k, v = prefill_inputs(sh, seed=21)
+    stats, oq, rho = gpu.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda())
+    ocfg = O.Cfg(n_layers=3, n_q_heads=8, n_kv_heads=2, head_dim=128, batch=2, window=32, budget_tokens=512)
+    rs, roq, rrho, _ = O.prefill_stats(_np(qw), _np(k), ocfg)
+    np.testing.assert_allclose(stats.cpu().numpy(), rs, rtol=STAT_RTOL)
+    np.testing.assert_allclose(oq.cpu().numpy(), roq, rtol=STAT_RTOL)
+    np.testing.assert_allclose(rho, rrho, rtol=STAT_RTOL)
+
+
+def test_decode_errors():
+    from paper_2603_08727_b200 import arkv as A
+    gpu, _, _ = make_pair(TOY, budget=32, steps=4)
+    q, kn, vn = decode_inputs(TOY, 0)
+    with pytest.raises(A.ArkvError) as e:
+        gpu.arkv_decode_step(q.cuda(), kn.cuda(), vn.cuda())
+    assert e.value.code == -3
+    qw, k, v = prefill_inputs(TOY)
+    gpu.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda(), rho_override=[[1.0]])
+    from paper_2603_08727_b200.arkv import lib, _ptr, _stream_ptr
+    out = torch.empty(q.shape, device="cuda")
+    rc = lib().arkv_decode_step(gpu.handle, 0, 1, _ptr(q.cuda()), _ptr(kn.cuda()), _ptr(vn.cuda()), 31, 4,
+                                _ptr(out), 1, _stream_ptr(None))
+    assert rc == -5
+
+
+def test_determinism_bitwise():
+    outs = []
+    for _ in range(2):
+        gpu, _, _ = make_pair(MID, budget=512, steps=40)
+        qw, k, v = prefill_inputs(MID, seed=4)
+        gpu.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda())
+        o = [gpu.arkv_decode_step(*[t.cuda() for t in decode_inputs(MID, s, seed=4)]).cpu() for s in range(40)]
+        outs.append((torch.stack(o), gpu.arkv_export_unit(0, 1, 1)))
+    assert torch.equal(outs[0][0], outs[1][0])
+    for key in ("state", "o_k", "q_k", "k_scale"):
+        np.testing.assert_array_equal(outs[0][1][key], outs[1][1][key])
