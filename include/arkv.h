@@ -194,6 +194,10 @@ arkv_status arkv_profile(arkv_cache* cache, int32_t enable);
 arkv_status arkv_profile_read(arkv_cache* cache, int32_t which, double* total_ms, int64_t* launches,
                               double* alg_bytes);
 
+/* Introspection: what = 0 -> tile layout in use (ARKV_LAYOUT_PLAIN / _FRAG);
+   1 -> decode kernel in use (0 generic, 1 tensor-core fast kernel).  -1 on error. */
+int32_t arkv_cache_info(const arkv_cache* cache, int32_t what);
+
 /* Number of kernel launches issued by this cache so far (bench accounting). */
 int64_t arkv_launch_count(const arkv_cache* cache);
 

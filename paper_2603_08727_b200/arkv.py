@@ -46,7 +46,8 @@ EXPORTED = [
     "arkv_config_default", "arkv_cache_bytes", "arkv_cache_create", "arkv_cache_destroy",
     "arkv_prefill_stats", "arkv_decode_step", "arkv_unit_counts", "arkv_export_unit",
     "arkv_check", "arkv_schedule", "arkv_oq_score", "arkv_launch_count", "arkv_version",
-    "arkv_status_string",
+    "arkv_status_string", "arkv_cache_info", "arkv_prefill_begin", "arkv_prefill_finish",
+    "arkv_profile", "arkv_profile_read",
 ]
 
 _lib = None
@@ -71,13 +72,19 @@ def lib() -> ctypes.CDLL:
         L.arkv_check.argtypes = [vp, vp]
         L.arkv_schedule.argtypes = [P(ArkvConfig), i32, dbl, i32, P(i32), i32, P(i32)]
         L.arkv_oq_score.argtypes = [P(ArkvConfig), dbl, dbl, dbl, P(dbl), P(dbl)]
+        L.arkv_cache_info.argtypes = [vp, i32]
+        L.arkv_cache_info.restype = ctypes.c_int32
+        L.arkv_prefill_begin.argtypes = [vp, vp, vp, i32, vp, vp]
+        L.arkv_prefill_finish.argtypes = [vp, vp, vp, i32, vp, vp, vp, vp, vp, vp]
+        L.arkv_profile.argtypes = [vp, i32]
+        L.arkv_profile_read.argtypes = [vp, i32, P(dbl), P(ctypes.c_int64), P(dbl)]
         L.arkv_launch_count.argtypes = [vp]
         L.arkv_launch_count.restype = ctypes.c_int64
         L.arkv_version.restype = ctypes.c_char_p
         L.arkv_status_string.restype = ctypes.c_char_p
         L.arkv_status_string.argtypes = [ctypes.c_int]
         for n in EXPORTED:
-            if n not in ("arkv_launch_count", "arkv_version", "arkv_status_string"):
+            if n not in ("arkv_launch_count", "arkv_version", "arkv_status_string", "arkv_cache_info"):
                 getattr(L, n).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -190,6 +197,44 @@ class ArkvCache:
         _ok(lib().arkv_prefill_stats(self.handle, _ptr(q_win), _ptr(k), _ptr(v), P, ro, _ptr(stats), _ptr(oq), rho,
                                      _stream_ptr(stream)), "arkv_prefill_stats")
         return stats, oq, np.array(rho[:]).reshape(B, L)
+
+    def arkv_prefill_begin(self, q_win, k, colsum=None, stream=None):
+        """Passes 1-2 and the local Eq. 3 column sums [B][L][max_positions] (float64)."""
+        import torch
+        B, L = self.cfg.batch, self.cfg.n_layers
+        if colsum is None:
+            colsum = torch.zeros(B, L, self.cfg.max_positions, dtype=torch.float64, device=self.device)
+        _ok(lib().arkv_prefill_begin(self.handle, _ptr(q_win), _ptr(k), k.shape[-2], _ptr(colsum),
+                                     _stream_ptr(stream)), "arkv_prefill_begin")
+        return colsum
+
+    def arkv_prefill_finish(self, k, v, colsum, rho_override=None, stats=None, oq=None, stream=None):
+        import torch
+        B, L = self.cfg.batch, self.cfg.n_layers
+        if stats is None:
+            stats = torch.empty(B, L, 3, dtype=torch.float64, device=self.device)
+        if oq is None:
+            oq = torch.empty(B, L, dtype=torch.float64, device=self.device)
+        rho = (ctypes.c_double * (B * L))()
+        ro = None
+        if rho_override is not None:
+            arr = np.asarray(rho_override, dtype=np.float64).reshape(B * L)
+            ro = (ctypes.c_double * (B * L))(*arr.tolist())
+        _ok(lib().arkv_prefill_finish(self.handle, _ptr(k), _ptr(v), k.shape[-2], _ptr(colsum), ro, _ptr(stats),
+                                      _ptr(oq), rho, _stream_ptr(stream)), "arkv_prefill_finish")
+        return stats, oq, np.array(rho[:]).reshape(B, L)
+
+    def arkv_profile(self, enable: bool):
+        _ok(lib().arkv_profile(self.handle, 1 if enable else 0), "arkv_profile")
+
+    def arkv_profile_read(self, which: int = 0):
+        ms, n, by = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+        _ok(lib().arkv_profile_read(self.handle, which, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(by)),
+            "arkv_profile_read")
+        return ms.value, n.value, by.value
+
+    def arkv_cache_info(self, what: int) -> int:
+        return int(lib().arkv_cache_info(self.handle, what))
 
     def arkv_decode_step(self, q, k, v, layer0=0, out=None, out_fp32=True, stream=None):
         import torch

@@ -385,6 +385,13 @@ arkv_status arkv_profile_read(arkv_cache* c, int32_t which, double* total_ms, in
 
 int64_t arkv_launch_count(const arkv_cache* c) { return c ? c->launches : 0; }
 
+int32_t arkv_cache_info(const arkv_cache* c, int32_t what) {
+  if (!c) return -1;
+  if (what == 0) return c->g.layout;
+  if (what == 1) return c->fast ? 1 : 0;
+  return -1;
+}
+
 // Runs a list of tailor jobs in waves bounded by the spare-slot count.
 static arkv_status run_jobs(arkv_cache* c, std::vector<TailorJob>& jobs, const uint16_t* pk, const uint16_t* pv, int P,
                             cudaStream_t s) {
