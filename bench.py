@@ -398,8 +398,14 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=256)
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prompt-len", type=int, default=0, help="debug: override the workload's prompt length")
+    ap.add_argument("--layers", type=int, default=0, help="debug: override the workload's layer count")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.prompt_len:
+        wl["prompt_len"] = args.prompt_len
+    if args.layers:
+        wl["n_layers"] = args.layers
     if args.impl == "reference":
         args.steps = min(args.steps, 128)   # each step is a bounded CPU sample (one layer-step)
         args.warmup = min(args.warmup, 4)

@@ -175,7 +175,18 @@ int64_t appends_to_trigger(const Geom& g, int64_t n_o, int64_t n_q) {
   return (Bb - U) / g.cost_o + 1;
 }
 
-bool check_cuda(cudaError_t e) { return e == cudaSuccess; }
+// ARKV_DEBUG_SYNC=1: synchronize after every launch group and name the failing one.
+void debug_sync(cudaStream_t s, const char* what) {
+  static const bool on = std::getenv("ARKV_DEBUG_SYNC") != nullptr;
+  if (!on) return;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) std::fprintf(stderr, "arkv: %s failed: %s\n", what, cudaGetErrorString(e));
+}
+
+bool check_cuda(cudaError_t e) {
+  if (e != cudaSuccess) std::fprintf(stderr, "arkv: CUDA error: %s\n", cudaGetErrorString(e));
+  return e == cudaSuccess;
+}
 
 }  // namespace
 
@@ -332,7 +343,7 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   c->unit_slot.resize(s.g.n_units);
   for (int u = 0; u < s.g.n_units; ++u) c->unit_slot[u] = u;
   for (int k = c->n_slots - 1; k >= s.g.n_units; --k) c->spare.push_back(k);
-  bool fast_ok = s.g.layout == ARKV_LAYOUT_FRAG && s.g.bits == 4 && s.g.d == 128;
+  bool fast_ok = decode_fast_available(s.g);
   c->fast = cfg->decode_kernel == 2 ? fast_ok : (cfg->decode_kernel == 0 ? fast_ok : false);
   if (cfg->decode_kernel == 2 && !fast_ok) {
     delete c;
@@ -420,6 +431,7 @@ static arkv_status run_jobs(arkv_cache* c, std::vector<TailorJob>& jobs, const u
                            c->src_scratch, c->err, s);
     if (nl < 0) return ARKV_ERR_CONFIG;
     c->launches += nl;
+    debug_sync(s, "tailor");
     if (!check_cuda(cudaGetLastError())) return ARKV_ERR_CUDA;
     for (int k = 0; k < n; ++k) {
       const TailorJob& jb = jobs[i + k];
@@ -444,6 +456,7 @@ arkv_status arkv_prefill_begin(arkv_cache* c, const void* q_win, const void* k, 
                                 d_colsum ? d_colsum : c->colsum, s);
   if (nl < 0) return ARKV_ERR_CONFIG;
   c->launches += nl;
+  debug_sync(s, "prefill_begin");
   if (!check_cuda(cudaGetLastError())) return ARKV_ERR_CUDA;
   return ARKV_OK;
 }
@@ -465,6 +478,7 @@ arkv_status arkv_prefill_finish(arkv_cache* c, const void* k, const void* v, int
     double* oq = d_oq ? d_oq : c->oq_tmp;
     int nl = launch_prefill_finish(g, d_colsum ? d_colsum : c->colsum, P, d_stats, oq, c->cfg.tau, c->cfg.stat_eps, s);
     c->launches += nl;
+    debug_sync(s, "prefill_finish");
     if (!check_cuda(cudaGetLastError())) return ARKV_ERR_CUDA;
     std::vector<double> h(BL);
     if (!check_cuda(cudaMemcpyAsync(h.data(), oq, BL * sizeof(double), cudaMemcpyDeviceToHost, s))) return ARKV_ERR_CUDA;
@@ -610,6 +624,7 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   }
   if (nl < 0) return ARKV_ERR_CONFIG;
   c->launches += nl;
+  debug_sync(s, "decode");
   if (!check_cuda(cudaGetLastError())) return ARKV_ERR_CUDA;
   for (int b = 0; b < g.batch; ++b)
     for (int l = layer0; l < layer0 + n_layers; ++l) {

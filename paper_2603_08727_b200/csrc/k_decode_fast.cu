@@ -1,7 +1,639 @@
-// k_decode_fast.cu — tensor-core decode attention for FRAG-layout caches (placeholder
-// until the mma.sync kernel lands; the generic kernel serves every cache meanwhile).
+// k_decode_fast.cu — tensor-core decode attention over O ∪ Q for FRAG-layout caches
+// (d = 128, 4-bit codes, G in {1,2,4,8}).  D1, D3, D7 of DESIGN.md §2.
+//
+// One CTA = one split of one unit: 1 producer warp + 4 consumer warps.
+//  * The producer streams whole 32-token tiles (16 KB Original, 4.5 KB Quantized)
+//    from HBM into a shared-memory ring with cp.async.bulk (the 1-D TMA engine,
+//    SASS UBLKCP) completing on mbarriers — no registers are spent on bytes in
+//    flight, and one CTA keeps up to kStages tiles in flight.
+//  * Consumer warp c takes tiles c, c+4, ...  The FRAG layout (common.cuh) stores
+//    every tile as lane-linear 16-byte quads, so each LDS.128 returns exactly a
+//    lane's mma.sync.m16n8k16 operand registers (no transposes, no bank conflicts).
+//      QK^T:  S[32 tok x 8] = K[32 x 128] · q^T    (M = tokens, N = heads padded to 8)
+//      PV:    O^T[128 x 8] += V^T[128 x 32] · P'^T (M = dims, N = heads x {hi, lo})
+//    Original tiles run bf16 x bf16; Quantized tiles run f16 x f16 on codes unpacked
+//    in registers with one LOP3 per two codes (fp16 "1024 + c" magic, minus 1024),
+//    the per-token scale/zero factored out of the contraction (x̃ = c·s + z,
+//    P:296-297): logit = s_k·(q·c) + z_k·Σq, and P' = p·s_v with Σ p·z_v added at
+//    the end.  P' is split into hi + lo halves (two columns each) so the 16-bit
+//    operand keeps ~22 bits, and is transposed from the QK accumulator layout into
+//    the PV operand layout with movmatrix.  Online softmax in the log2 domain.
+//  * HH accumulation (Eq. 9, R19): in the W steps before a tailor the logits are
+//    written out for the combine kernel; the new token (D1) is appended by the CTA
+//    owning the last Original tile and folded into its partial.
 #include "kernels.h"
 
 namespace arkv {
-int launch_decode_fast(const DecodeArgs&, int, cudaStream_t, cudaEvent_t, cudaEvent_t) { return -1; }
+
+namespace fast {
+
+constexpr int D = 128;
+constexpr int kConsumers = 4;
+// One ring stage per consumer warp (tile i -> warp i % 4 -> stage i % 4): every stage's
+// mbarriers are then waited on strictly in phase order by a single warp.  (With more
+// stages than warps a fast warp could wait on a stage two phases ahead, where
+// try_wait.parity reports the preceding phase as complete.)  64 KB ring: 2 CTAs/SM.
+constexpr int kStages = kConsumers;
+constexpr int kStageBytes = 32 * 4 * D;  // one Original tile (16 KB) — the largest
+constexpr int kThreads = (kConsumers + 1) * 32;
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ---- PTX helpers ------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t movtrans(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(d) : "r"(a));
+  return d;
+}
+__device__ __forceinline__ uint32_t lop3_mask_or(uint32_t a, uint32_t mask, uint32_t orv) {
+  uint32_t d;
+  asm volatile("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(d) : "r"(a), "r"(mask), "r"(orv));  // (a & b) | c
+  return d;
+}
+__device__ __forceinline__ uint32_t hsub2_1024(uint32_t x) {
+  uint32_t d;
+  const uint32_t m = 0x64006400u;
+  asm volatile("sub.f16x2 %0, %1, %2;\n" : "=r"(d) : "r"(x), "r"(m));
+  return d;
+}
+// 8 nibbles -> four f16x2 code pairs (exact small integers): (n0,n4), 16(n1,n5), (n2,n6), 16(n3,n7)
+__device__ __forceinline__ void unpack8(uint32_t w, uint32_t (&x)[4]) {
+  const uint32_t w8 = w >> 8;
+  x[0] = hsub2_1024(lop3_mask_or(w, 0x000F000Fu, 0x64006400u));
+  x[1] = hsub2_1024(lop3_mask_or(w, 0x00F000F0u, 0x64006400u));
+  x[2] = hsub2_1024(lop3_mask_or(w8, 0x000F000Fu, 0x64006400u));
+  x[3] = hsub2_1024(lop3_mask_or(w8, 0x00F000F0u, 0x64006400u));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *(uint32_t*)&v;
+}
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *(uint32_t*)&v;
+}
+__device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ float f16_round(float x) { return __half2float(__float2half_rn(x)); }
+__device__ __forceinline__ uint32_t word(const uint4& q, int i) { return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w; }
+
+struct Smem {
+  uint8_t ring[kStages][kStageBytes];
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  float wm[kConsumers][8];            // per warp, per head: running max (log2 domain)
+  float wl[kConsumers][8];            // sum of p
+  float wz[kConsumers][8][4];         // Σ p·z_v per head, per group
+  float newtok[3][8];                 // new token: logit per head (log2), valid flag
+};
+
+// Converts the fp32 P' block (thread holds rows gq, gq+8 x cols 2t, 2t+1) into the PV
+// B operand: columns [hi heads | lo heads] for 2G <= 8, transposed with movmatrix.
+template <int G, bool BF16>
+__device__ __forceinline__ void make_b(const float (&v)[4], int t, uint32_t& b01, uint32_t& b23, uint32_t& c01,
+                                       uint32_t& c23) {
+  // v: [0] (row g, col 2t) [1] (row g, col 2t+1) [2] (row g+8, col 2t) [3] (row g+8, col 2t+1)
+  float hi[4], lo[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    hi[i] = BF16 ? bf16_round(v[i]) : f16_round(v[i]);
+    lo[i] = v[i] - hi[i];
+  }
+  auto pk = [](float a, float b) { return BF16 ? pack_bf16(a, b) : pack_f16(a, b); };
+  uint32_t h0 = pk(hi[0], hi[1]), h1 = pk(hi[2], hi[3]);
+  uint32_t l0 = pk(lo[0], lo[1]), l1 = pk(lo[2], lo[3]);
+  if (G == 8) {
+    b01 = movtrans(h0);
+    b23 = movtrans(h1);
+    c01 = movtrans(l0);
+    c23 = movtrans(l1);
+    return;
+  }
+  uint32_t r0, r1;
+  if (G == 4) {
+    uint32_t s0 = __shfl_xor_sync(0xffffffffu, l0, 2), s1 = __shfl_xor_sync(0xffffffffu, l1, 2);
+    r0 = t < 2 ? h0 : s0;
+    r1 = t < 2 ? h1 : s1;
+  } else if (G == 2) {
+    uint32_t s0 = __shfl_sync(0xffffffffu, l0, (threadIdx.x & 28)), s1 = __shfl_sync(0xffffffffu, l1, (threadIdx.x & 28));
+    r0 = t == 0 ? h0 : (t == 1 ? s0 : 0u);
+    r1 = t == 0 ? h1 : (t == 1 ? s1 : 0u);
+  } else {  // G == 1: columns (hi h0, lo h0)
+    r0 = t == 0 ? pk(hi[0], lo[0]) : 0u;
+    r1 = t == 0 ? pk(hi[2], lo[2]) : 0u;
+  }
+  b01 = movtrans(r0);
+  b23 = movtrans(r1);
+  c01 = c23 = 0u;
+}
+
+template <int G, int NG>
+__global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const Geom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  // unit of this CTA
+  const int ul = blockIdx.y;
+  const int b = ul / (a.n_layers * g.Hkv);
+  const int rem = ul % (a.n_layers * g.Hkv);
+  const int li = rem / g.Hkv, kvh = rem % g.Hkv;
+  const int u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
+  const UnitDesc dsc = a.desc[u];
+  uint8_t* slot = a.slots + (int64_t)dsc.slot * g.slot_bytes;
+  const int n_o = dsc.n_o, n_q = dsc.n_q, t_pos = dsc.t_next;
+  const bool accm = (t_pos >= dsc.trig - g.W) && (t_pos < dsc.trig);
+  const int tiles_o = (n_o + 1 + kTile - 1) / kTile;
+  const int tiles_q = (n_q + kTile - 1) / kTile;
+  const int S = a.n_splits, s = blockIdx.x;
+  const int o0 = (int)((int64_t)s * tiles_o / S), o1 = (int)((int64_t)(s + 1) * tiles_o / S);
+  const int q0 = (int)((int64_t)s * tiles_q / S), q1 = (int)((int64_t)(s + 1) * tiles_q / S);
+  const int n_work = (o1 - o0) + (q1 - q0);
+  const bool owns_new = (o0 <= n_o / kTile) && (n_o / kTile < o1);
+  const int row_stride = g.cap_o + g.cap_q;
+  const int64_t qkv = (int64_t)(b * a.n_layers + li);
+  const uint16_t* qp = a.q + (qkv * g.Hq + kvh * G) * D;
+  const uint16_t* kn = a.k + (qkv * g.Hkv + kvh) * D;
+  const uint16_t* vn = a.v + (qkv * g.Hkv + kvh) * D;
+  const float c2 = g.sm_scale * kLog2e;
+  const bool sym = g.mode == ARKV_QUANT_SYM;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumers) {
+    // ===================== producer =====================
+    if (lane == 0) {
+      for (int i = 0; i < n_work; ++i) {
+        const int st = i % kStages;
+        if (i >= kStages) mbar_wait(&sm.empty[st], ((i / kStages) - 1) & 1);
+        const bool isq = i >= (o1 - o0);
+        const uint8_t* src = isq ? q_tile_ptr(slot, g, q0 + (i - (o1 - o0))) : o_tile_ptr(slot, g, o0 + i);
+        const uint32_t bytes = isq ? (uint32_t)g.tile_q : (uint32_t)g.tile_o;
+        mbar_expect_tx(&sm.full[st], bytes);
+        bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
+      }
+    }
+    __syncwarp();  // reconverge before warp-collective code and the aligned CTA barrier
+    // the producer warp also appends the step's token (D1) when this CTA owns its tile
+    if (owns_new) {
+      const int tt = n_o / kTile, j = n_o % kTile;
+      const SlotMeta meta = slot_meta(a.meta, g, dsc.slot);
+      const bool fits = (n_o + 1 <= g.cap_o) &&
+                        ((int64_t)tiles_o * g.tile_o + (int64_t)tiles_q * g.tile_q <= g.slot_bytes);
+      if (!fits) {
+        if (lane == 0) atomicOr(a.err, kErrCapacity);
+      } else {
+        uint8_t* tb = o_tile_ptr(slot, g, tt);
+        for (int x = lane; x < D; x += 32) {
+          *(uint16_t*)(tb + o_k_off(g, j, x)) = kn[x];
+          *(uint16_t*)(tb + o_v_off(g, j, x)) = vn[x];
+        }
+        if (lane == 0) {
+          meta.pos_o[n_o] = t_pos;
+          meta.acc_o[n_o] = make_float2(0.f, 0.f);
+        }
+      }
+      // its logits (log2 domain) for the G heads
+      float kx[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) kx[i] = bf16_to_f(kn[lane * 4 + i]);
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc = fmaf(bf16_to_f(qp[h * D + lane * 4 + i]), kx[i], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) sm.newtok[0][h] = acc * c2;
+      }
+      if (accm && lane < G)
+        a.logits[((int64_t)u * G + lane) * row_stride + n_o] = sm.newtok[0][lane];
+    }
+  } else {
+    // ===================== consumers =====================
+    // q fragments: bf16 for Original tiles; f16 (with the 1/16 odd-nibble factor) for
+    // Quantized tiles; Σq per group for the zero-point term.
+    uint32_t qb[8][2], qh[8][2];
+    float qsum[2][NG];  // this thread's two heads (2t, 2t+1) — only lanes with tq < G/2 matter
+    {
+      const int hq = gq;  // B operand column n = head gq
+      const bool hv = hq < G;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int x0 = tq * 32 + 4 * c;  // Original tiles: dims t*(d/4)+4c+{0,1} / +{2,3}
+        qb[c][0] = hv ? *(const uint32_t*)(qp + hq * D + x0) : 0u;
+        qb[c][1] = hv ? *(const uint32_t*)(qp + hq * D + x0 + 2) : 0u;
+        // Quantized tiles: chunk c = 2jp + cc; nibble pairs (e, e+4) with e = 2cc (+1 for b1)
+        const int jp = c >> 1, cc = c & 1;
+        const int xb = 32 * jp + 8 * tq + 2 * cc;
+        float f0 = hv ? bf16_to_f(qp[hq * D + xb + 0]) : 0.f, f4 = hv ? bf16_to_f(qp[hq * D + xb + 4]) : 0.f;
+        float f1 = hv ? bf16_to_f(qp[hq * D + xb + 1]) : 0.f, f5 = hv ? bf16_to_f(qp[hq * D + xb + 5]) : 0.f;
+        qh[c][0] = pack_f16(f0, f4);
+        qh[c][1] = pack_f16(f1 * 0.0625f, f5 * 0.0625f);
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int h = 2 * tq + e;
+#pragma unroll
+        for (int gr = 0; gr < NG; ++gr) {
+          float sacc = 0.f;
+          if (h < G)
+            for (int x = gr * (D / NG); x < (gr + 1) * (D / NG); ++x) sacc += bf16_to_f(qp[h * D + x]);
+          qsum[e][gr] = sacc;
+        }
+      }
+    }
+    float o[8][4];  // O^T accumulators: m-tile over dims, (dim g|g+8) x (col 2t|2t+1)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[i][e] = 0.f;
+    float m_run[2] = {-INFINITY, -INFINITY};  // heads 2t, 2t+1
+    float l_run[2] = {0.f, 0.f};
+    float z_run[2][NG];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int gr = 0; gr < NG; ++gr) z_run[e][gr] = 0.f;
+    // lane holding the running max of the heads of this thread's O^T columns
+    const int src_t = G >= 2 ? ((2 * tq) % G) / 2 : 0;
+    const int src_lane = (lane & ~3) | src_t;
+
+    for (int i = warp; i < n_work; i += kConsumers) {
+      const int st = i % kStages;
+      mbar_wait(&sm.full[st], (i / kStages) & 1);
+      __syncwarp();  // lanes may leave the spin-wait in different iterations; mma/movmatrix are .aligned
+      const uint8_t* tb = sm.ring[st];
+      const bool isq = i >= (o1 - o0);
+      const int tile = isq ? q0 + (i - (o1 - o0)) : o0 + i;
+      const int n_valid = isq ? min(kTile, n_q - tile * kTile) : min(kTile, n_o - tile * kTile);
+
+      // ---- S = K q^T, logits in the log2 domain ----
+      float lg[2][4];  // [m-tile][(row g|g+8) x (col 2t|2t+1)]
+      float zv[2][2][NG];  // Quantized: z_v of rows (g, g+8) per m-tile, per group
+      if (!isq) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) {
+            const uint4 r0 = lds128(tb + (((mt * 2 + 0) * 4 + qd) * 32 + lane) * 16);
+            const uint4 r1 = lds128(tb + (((mt * 2 + 1) * 4 + qd) * 32 + lane) * 16);
+            mma_bf16(acc, r0.x, r1.x, r0.y, r1.y, qb[2 * qd][0], qb[2 * qd][1]);
+            mma_bf16(acc, r0.z, r1.z, r0.w, r1.w, qb[2 * qd + 1][0], qb[2 * qd + 1][1]);
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) lg[mt][e] = acc[e] * c2;
+        }
+      } else {
+        const float* sc = (const float*)(tb + 32 * D);  // [which][grp][32]
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          float acc[NG][4];
+#pragma unroll
+          for (int gr = 0; gr < NG; ++gr)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[gr][e] = 0.f;
+          const uint4 r0 = lds128(tb + ((mt * 2 + 0) * 32 + lane) * 16);
+          const uint4 r1 = lds128(tb + ((mt * 2 + 1) * 32 + lane) * 16);
+#pragma unroll
+          for (int jp = 0; jp < 4; ++jp) {
+            uint32_t x[4], y[4];
+            unpack8(word(r0, jp), x);
+            unpack8(word(r1, jp), y);
+            const int gr = (jp * 32) / (D / NG);
+            mma_f16(acc[gr], x[0], y[0], x[1], y[1], qh[2 * jp][0], qh[2 * jp][1]);
+            mma_f16(acc[gr], x[2], y[2], x[3], y[3], qh[2 * jp + 1][0], qh[2 * jp + 1][1]);
+          }
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int j = mt * 16 + gq + 8 * hh;
+            float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+            for (int gr = 0; gr < NG; ++gr) {
+              const float ks = sc[(0 * NG + gr) * 32 + j];
+              float kz = sc[(1 * NG + gr) * 32 + j];
+              const float vs = sc[(2 * NG + gr) * 32 + j];
+              float vz = sc[(3 * NG + gr) * 32 + j];
+              if (sym) {
+                kz = -8.f * ks;
+                vz = -8.f * vs;
+              }
+              l0 += ks * acc[gr][hh * 2 + 0] + kz * qsum[0][gr];
+              l1 += ks * acc[gr][hh * 2 + 1] + kz * qsum[1][gr];
+              zv[mt][hh][gr] = vz;
+            }
+            lg[mt][hh * 2 + 0] = l0 * c2;
+            lg[mt][hh * 2 + 1] = l1 * c2;
+          }
+        }
+      }
+      // mask rows beyond the segment (and padding heads)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = mt * 16 + gq + 8 * (e >> 1);
+          const int h = 2 * tq + (e & 1);
+          if (j >= n_valid || h >= G) lg[mt][e] = -INFINITY;
+        }
+      if (accm) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = mt * 16 + gq + 8 * (e >> 1);
+            const int h = 2 * tq + (e & 1);
+            if (j < n_valid && h < G)
+              a.logits[((int64_t)u * G + h) * row_stride + (isq ? g.cap_o : 0) + tile * kTile + j] = lg[mt][e];
+          }
+      }
+      // ---- online softmax (per head = per (tq, e)) ----
+      float tmax[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        float mx = fmaxf(fmaxf(lg[0][e], lg[0][e + 2]), fmaxf(lg[1][e], lg[1][e + 2]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        tmax[e] = mx;
+      }
+      float corr[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float mn = fmaxf(m_run[e], tmax[e]);
+        corr[e] = (mn == -INFINITY) ? 1.f : exp2f(m_run[e] - mn);
+        m_run[e] = mn;
+        l_run[e] *= corr[e];
+#pragma unroll
+        for (int gr = 0; gr < NG; ++gr) z_run[e][gr] *= corr[e];
+      }
+      // rescale O^T columns: col 2t+e belongs to head (2t+e) % G, whose max lives in lane src_lane
+      {
+        const float c0 = __shfl_sync(0xffffffffu, corr[0], src_lane);
+        const float c1 = __shfl_sync(0xffffffffu, G >= 2 ? corr[1] : corr[0], src_lane);
+#pragma unroll
+        for (int mv = 0; mv < 8; ++mv) {
+          o[mv][0] *= c0;
+          o[mv][1] *= c1;
+          o[mv][2] *= c0;
+          o[mv][3] *= c1;
+        }
+      }
+      float p[2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float mm = m_run[e & 1];
+          p[mt][e] = (lg[mt][e] == -INFINITY) ? 0.f : exp2f(lg[mt][e] - mm);
+          l_run[e & 1] += p[mt][e];
+        }
+
+      if (!isq) {
+        // ---- PV on Original tiles (bf16) ----
+        if (n_valid < kTile) {
+          // rows past the segment may hold never-written bytes (NaN patterns): P' = 0
+          // there, but 0 * NaN = NaN inside the MMA, so zero them in the staged copy
+          uint8_t* tw = const_cast<uint8_t*>(tb);
+          for (int idx = lane; idx < (kTile - n_valid) * D; idx += 32)
+            *(uint16_t*)(tw + o_v_off(g, n_valid + idx / D, idx % D)) = 0;
+          // order these generic-proxy writes before the stage's next TMA (async-proxy) fill
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          __syncwarp();
+        }
+        uint32_t b01[2], b23[2], c01[2], c23[2];
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) make_b<G, true>(p[kc], tq, b01[kc], b23[kc], c01[kc], c23[kc]);
+        const uint8_t* vb = tb + 64 * D;
+#pragma unroll
+        for (int mv = 0; mv < 8; ++mv) {
+#pragma unroll
+          for (int kc = 0; kc < 2; ++kc) {
+            const uint4 r = lds128(vb + ((mv * 2 + kc) * 32 + lane) * 16);
+            mma_bf16(o[mv], r.x, r.y, r.z, r.w, b01[kc], b23[kc]);
+            if (G == 8) mma_bf16(o[mv], r.x, r.y, r.z, r.w, c01[kc], c23[kc]);
+          }
+        }
+      } else {
+        // ---- PV on Quantized tiles (f16 codes, P' = p·s_v / f) ----
+        const float* sc = (const float*)(tb + 32 * D);
+        uint32_t b01[NG][2], b23[NG][2], c01[NG][2], c23[NG][2];
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) {
+#pragma unroll
+          for (int gr = 0; gr < NG; ++gr) {
+            float vsc[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) vsc[hh] = sc[(2 * NG + gr) * 32 + kc * 16 + gq + 8 * hh];
+            float pv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pv[e] = p[kc][e] * vsc[e >> 1] * ((e >> 1) ? 0.0625f : 1.f);
+            make_b<G, false>(pv, tq, b01[gr][kc], b23[gr][kc], c01[gr][kc], c23[gr][kc]);
+            // zero-point term Σ p·z_v
+#pragma unroll
+            for (int e = 0; e < 4; ++e) z_run[e & 1][gr] += p[kc][e] * zv[kc][e >> 1][gr];
+          }
+        }
+        const uint8_t* vb = tb + 16 * D;
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+          const uint4 r = lds128(vb + (qd * 32 + lane) * 16);
+#pragma unroll
+          for (int hm = 0; hm < 2; ++hm) {
+            const int mv = 2 * qd + hm;
+            const int gr = (mv * 16) / (D / NG);
+            uint32_t x[4], y[4];
+            unpack8(word(r, 2 * hm + 0), x);  // dim row g
+            unpack8(word(r, 2 * hm + 1), y);  // dim row g+8
+#pragma unroll
+            for (int kc = 0; kc < 2; ++kc) {
+              mma_f16(o[mv], x[2 * kc], y[2 * kc], x[2 * kc + 1], y[2 * kc + 1], b01[gr][kc], b23[gr][kc]);
+              if (G == 8)
+                mma_f16(o[mv], x[2 * kc], y[2 * kc], x[2 * kc + 1], y[2 * kc + 1], c01[gr][kc], c23[gr][kc]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[st]);
+    }
+
+    // ---- per-warp finalisation: reduce l and z over the 8 row lanes ----
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        l_run[e] += __shfl_xor_sync(0xffffffffu, l_run[e], off);
+#pragma unroll
+        for (int gr = 0; gr < NG; ++gr) z_run[e][gr] += __shfl_xor_sync(0xffffffffu, z_run[e][gr], off);
+      }
+    }
+    if (gq == 0) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int h = 2 * tq + e;
+        if (h < G) {
+          sm.wm[warp][h] = m_run[e];
+          sm.wl[warp][h] = l_run[e];
+#pragma unroll
+          for (int gr = 0; gr < NG; ++gr) sm.wz[warp][h][gr] = z_run[e][gr];
+        }
+      }
+    }
+    // every consumer is done with the ring: reuse it for the O^T accumulators
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumers * 32) : "memory");
+    float* ob = (float*)sm.ring[0] + warp * 8 * D;  // [col][dim]
+#pragma unroll
+    for (int mv = 0; mv < 8; ++mv) {
+      const int x0 = mv * 16 + gq;
+      ob[(2 * tq + 0) * D + x0] = o[mv][0];
+      ob[(2 * tq + 1) * D + x0] = o[mv][1];
+      ob[(2 * tq + 0) * D + x0 + 8] = o[mv][2];
+      ob[(2 * tq + 1) * D + x0 + 8] = o[mv][3];
+    }
+  }
+  __syncthreads();
+  // ---- CTA merge of the consumer warps (+ the appended token) -> split partial ----
+  const float* ob = (const float*)sm.ring[0];
+  float* part = a.partials + ((int64_t)u * a.max_splits + s) * G * (D + 2);
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int h = idx / D, x = idx % D;
+    const int gr = x / (D / NG);
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kConsumers; ++w) M = fmaxf(M, sm.wm[w][h]);
+    float snew = -INFINITY;
+    if (owns_new) {
+      snew = sm.newtok[0][h];
+      M = fmaxf(M, snew);
+    }
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < kConsumers; ++w) {
+      const float mw = sm.wm[w][h];
+      if (mw == -INFINITY) continue;
+      const float cw = exp2f(mw - M);
+      float ow = ob[(w * 8 + h) * D + x];
+      if (G < 8) ow += ob[(w * 8 + h + G) * D + x];
+      ow += sm.wz[w][h][gr];
+      L += sm.wl[w][h] * cw;
+      O += ow * cw;
+    }
+    if (owns_new) {
+      const float cn = exp2f(snew - M);
+      L += cn;
+      O += cn * bf16_to_f(vn[x]);
+    }
+    part[h * (D + 2) + 2 + x] = O;
+    if (x == 0) {
+      part[h * (D + 2) + 0] = M;
+      part[h * (D + 2) + 1] = L;
+    }
+  }
+}
+
+template <int G, int NG>
+static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+  auto kern = decode_fast_kernel<G, NG>;
+  const int smem = (int)sizeof(Smem);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  dim3 grid(a.n_splits, n_units_call);
+  if (ev0) cudaEventRecord(ev0, s);
+  kern<<<grid, kThreads, smem, s>>>(a);
+  if (ev1) cudaEventRecord(ev1, s);
+}
+
+template <int G>
+static int launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+  switch (a.g.ng) {
+    case 1: launch_gn<G, 1>(a, n_units_call, s, ev0, ev1); return 0;
+    case 2: launch_gn<G, 2>(a, n_units_call, s, ev0, ev1); return 0;
+    case 4: launch_gn<G, 4>(a, n_units_call, s, ev0, ev1); return 0;
+    default: return -1;
+  }
+}
+
+}  // namespace fast
+
+bool decode_fast_available(const Geom& g) {
+  return g.layout == ARKV_LAYOUT_FRAG && g.d == fast::D && g.bits == 4 && (g.ng == 1 || g.ng == 2 || g.ng == 4) &&
+         (g.G == 1 || g.G == 2 || g.G == 4 || g.G == 8);
+}
+
+void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s);  // k_decode.cu
+
+int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+  if (!decode_fast_available(a.g)) return -1;
+  int r = -1;
+  switch (a.g.G) {
+    case 1: r = fast::launch_g<1>(a, n_units_call, s, ev0, ev1); break;
+    case 2: r = fast::launch_g<2>(a, n_units_call, s, ev0, ev1); break;
+    case 4: r = fast::launch_g<4>(a, n_units_call, s, ev0, ev1); break;
+    case 8: r = fast::launch_g<8>(a, n_units_call, s, ev0, ev1); break;
+    default: return -1;
+  }
+  if (r < 0) return -1;
+  launch_decode_combine(a, n_units_call, s);
+  return 2;
+}
+
 }  // namespace arkv

@@ -63,3 +63,8 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
                   cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
 }  // namespace arkv
+
+namespace arkv {
+// k_decode_fast.cu: true when the tensor-core decode kernel supports this cache.
+bool decode_fast_available(const Geom& g);
+}  // namespace arkv
