@@ -35,6 +35,9 @@ struct arkv_cache {
   float2* acc_pf = nullptr;
   double* oq_tmp = nullptr;
   double* colsum = nullptr;
+  float* mstat = nullptr;
+  int32_t* counters = nullptr;
+  int num_sms = 148;
   int jobs_per_wave = 0, max_splits = 64, n_chunks1_max = 1;
   // live kernel timing of the decode attention kernel (bench roofline)
   bool prof = false;
@@ -62,7 +65,7 @@ struct Sizes {
   int n_spare, jobs_per_wave, max_splits, n_chunks1;
   int64_t arena, ws;
   int64_t off_meta, off_desc, off_err;
-  int64_t w_partials, w_logits, w_st, w_src, w_pfp, w_accpf, w_oq, w_colsum;
+  int64_t w_partials, w_logits, w_st, w_src, w_pfp, w_accpf, w_oq, w_colsum, w_mstat, w_counters;
 };
 
 int64_t cost_o(const arkv_config& c) { return 4LL * c.head_dim; }
@@ -152,6 +155,10 @@ Sizes compute_sizes(const arkv_config& c) {
   w = round_up(w + (int64_t)g.batch * g.L * 8, 256);
   s.w_colsum = w;
   w = round_up(w + (int64_t)g.batch * g.L * g.max_pos * 8, 256);
+  s.w_mstat = w;
+  w = round_up(w + (int64_t)g.n_units * g.G * 8, 256);
+  s.w_counters = w;
+  w = round_up(w + (int64_t)g.n_units * 4, 256);
   s.ws = w;
   return s;
 }
@@ -331,6 +338,9 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   c->acc_pf = (float2*)(w + s.w_accpf);
   c->oq_tmp = (double*)(w + s.w_oq);
   c->colsum = (double*)(w + s.w_colsum);
+  c->mstat = (float*)(w + s.w_mstat);
+  c->counters = (int32_t*)(w + s.w_counters);
+  c->num_sms = prop.multiProcessorCount;
   c->jobs_per_wave = s.jobs_per_wave;
   c->max_splits = s.max_splits;
   c->n_chunks1_max = s.n_chunks1;
@@ -349,7 +359,7 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
     delete c;
     return ARKV_ERR_CONFIG;
   }
-  if (!check_cuda(cudaMemset(c->err, 0, 4))) {
+  if (!check_cuda(cudaMemset(c->err, 0, 4)) || !check_cuda(cudaMemset(c->counters, 0, (size_t)s.g.n_units * 4))) {
     delete c;
     return ARKV_ERR_CUDA;
   }
@@ -557,7 +567,8 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   if (!c->prefilled) return ARKV_ERR_SEQUENCE;
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<TailorJob> jobs;
-  int max_tiles = 1;
+  int max_tiles = 1, acc_rows = 0;
+  double max_bytes = 0.0;
   for (int b = 0; b < g.batch; ++b)
     for (int l = layer0; l < layer0 + n_layers; ++l) {
       const int bl = b * g.L + l;
@@ -590,15 +601,34 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
       }
       const int tiles = (c->n_o[bl] + 1 + kTile - 1) / kTile + (c->n_q[bl] + kTile - 1) / kTile;
       max_tiles = std::max(max_tiles, tiles);
+      max_bytes = std::max(max_bytes, (double)(c->n_o[bl] + 1) * g.cost_o + (double)c->n_q[bl] * g.cost_q);
+      if (t >= c->trig[bl] - g.W && t < c->trig[bl])  // HH accumulation step (R19)
+        acc_rows = std::max(acc_rows, c->n_o[bl] + 1 + c->n_q[bl]);
     }
   if (!jobs.empty()) {
     arkv_status st = run_jobs(c, jobs, nullptr, nullptr, 0, s);
     if (st != ARKV_OK) return st;
   }
-  // split-K fan-out: ~4 CTAs per SM in flight, never more splits than tiles
+  // split-K fan-out: minimise the wave-quantised time ceil(units*S/slots) * (1/S + f),
+  // f = per-CTA fixed cost relative to streaming a whole unit; never more splits than tiles
   const int n_units_call = g.batch * n_layers * g.Hkv;
-  int S = (4 * 148 + n_units_call - 1) / n_units_call;
-  S = std::max(1, std::min(S, std::min(c->max_splits, max_tiles)));
+  const int slots = c->num_sms * (c->fast ? 2 : 4);
+  const double per_cta_bw = 5.0e12 / slots, t_fixed = 6.0e-6;  // measured sweep: S = 2..3 at configs[1]
+  const double f = t_fixed / std::max(max_bytes / per_cta_bw, 1e-9);
+  int S = 1;
+  double best = 1e300;
+  for (int cand = 1; cand <= std::min(c->max_splits, max_tiles); ++cand) {
+    const double waves = std::ceil((double)n_units_call * cand / slots);
+    const double cost = waves * (1.0 / cand + f);
+    if (cost < best - 1e-12) {
+      best = cost;
+      S = cand;
+    }
+  }  if (const char* env = std::getenv("ARKV_SPLITS")) {  // tuning knob (bench sweeps)
+    const int v = std::atoi(env);
+    if (v > 0) S = std::min(v, std::min(c->max_splits, max_tiles));
+  }
+
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->prof && 2 * (c->ev_used + 1) <= (int)c->ev.size()) {
     e0 = c->ev[2 * c->ev_used];
@@ -616,11 +646,12 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
     c->ev_used++;
   }
   int nl = launch_decode(g, layer0, n_layers, (const uint16_t*)q, (const uint16_t*)k, (const uint16_t*)v, out,
-                         out_fp32, c->slots, c->meta, c->desc, c->partials, c->logits, S, c->max_splits, c->fast ? 1 : 0,
-                         c->err, s, e0, e1);
+                         out_fp32, c->slots, c->meta, c->desc, c->partials, c->logits, c->mstat, c->counters, acc_rows, S,
+                         c->max_splits, c->fast ? 1 : 0, c->err, s, e0, e1);
   if (nl < 0 && c->fast) {  // fast kernel not available for this shape: generic kernel
     nl = launch_decode(g, layer0, n_layers, (const uint16_t*)q, (const uint16_t*)k, (const uint16_t*)v, out, out_fp32,
-                       c->slots, c->meta, c->desc, c->partials, c->logits, S, c->max_splits, 0, c->err, s, e0, e1);
+                       c->slots, c->meta, c->desc, c->partials, c->logits, c->mstat, c->counters, acc_rows, S, c->max_splits, 0,
+                       c->err, s, e0, e1);
   }
   if (nl < 0) return ARKV_ERR_CONFIG;
   c->launches += nl;

@@ -10,7 +10,9 @@
 // the next tailor (Eq. 9 / R19) from the logits the split kernel kept, and advances
 // the unit descriptor.  This generic kernel handles every layout/shape; the fast
 // tensor-core kernel (k_decode_fast.cu) takes FRAG-layout 4-bit d=128 caches.
-#include "kernels.h"
+#include <cstdlib>
+
+#include "combine.cuh"
 
 namespace arkv {
 
@@ -231,73 +233,63 @@ __global__ void __launch_bounds__(128) decode_split_generic(DecodeArgs a) {
 // Combine: merge split partials, write the output, HH accumulation, advance the unit.
 template <int G>
 __global__ void __launch_bounds__(256) decode_combine(DecodeArgs a) {
-  const Geom& g = a.g;
-  const int d = g.d;
   int b, li, kvh, u;
   unit_of(a, blockIdx.x, b, li, kvh, u);
   const UnitDesc dsc = a.desc[u];
-  const int S = a.n_splits;
   __shared__ float sM[G], sIL[G];
-  const float* part = a.partials + (int64_t)u * a.max_splits * G * (d + 2);
-  if (threadIdx.x < G) {
-    int h = threadIdx.x;
-    float M = -INFINITY;
-    for (int s = 0; s < S; ++s) M = fmaxf(M, part[(s * G + h) * (d + 2)]);
-    float L = 0.f;
-    for (int s = 0; s < S; ++s) {
-      float ms = part[(s * G + h) * (d + 2)];
-      if (ms != -INFINITY) L += part[(s * G + h) * (d + 2) + 1] * exp2f(ms - M);
-    }
-    sM[h] = M;
-    sIL[h] = 1.0f / L;
-  }
-  __syncthreads();
-  const int64_t obase = ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * G) * d;
-  for (int idx = threadIdx.x; idx < G * d; idx += blockDim.x) {
-    int h = idx / d, x = idx % d;
-    float O = 0.f;
-    for (int s = 0; s < S; ++s) {
-      float ms = part[(s * G + h) * (d + 2)];
-      if (ms != -INFINITY) O += part[(s * G + h) * (d + 2) + 2 + x] * exp2f(ms - sM[h]);
-    }
-    O *= sIL[h];
-    if (a.out_fp32)
-      ((float*)a.out)[obase + idx] = O;
-    else
-      ((uint16_t*)a.out)[obase + idx] = f_to_bf16_rne(O);
-  }
-  const int t = dsc.t_next;
-  const bool accm = (t >= dsc.trig - g.W) && (t < dsc.trig);
-  if (accm) {
-    const bool first = t == dsc.trig - g.W;
-    const SlotMeta sm = slot_meta(a.meta, g, dsc.slot);
-    const int row_stride = g.cap_o + g.cap_q;
-    const int n_rows = dsc.n_o + 1 + dsc.n_q;
-    for (int i = threadIdx.x; i < n_rows; i += blockDim.x) {
-      const bool isq = i > dsc.n_o;
-      const int ridx = isq ? g.cap_o + (i - dsc.n_o - 1) : i;
-      float a1 = 0.f, a2 = 0.f;
+  combine_unit<G>(a, u, b, li, kvh, dsc, sM, sIL);
+}
+
+// Heavy-hitter accumulation (Eq. 9, D3; R19): in the W steps before a unit's next
+// tailor, every cached row gets acc1 += Σ_h p, acc2 += Σ_h p² with p = 2^(s - M) / L
+// from the step's logits and the merged row statistics.  Launched after the combine
+// (the descriptor already counts the appended token); one thread per row.
+template <int G>
+__global__ void __launch_bounds__(256) decode_hh_acc(DecodeArgs a) {
+  const Geom& g = a.g;
+  int b, li, kvh, u;
+  unit_of(a, blockIdx.y, b, li, kvh, u);
+  const UnitDesc dsc = a.desc[u];
+  const int t = dsc.t_next - 1;  // the step just attended
+  if (!((t >= dsc.trig - g.W) && (t < dsc.trig))) return;
+  const bool first = t == dsc.trig - g.W;
+  const int n_rows = dsc.n_o + dsc.n_q;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_rows) return;
+  float M[G], IL[G];
 #pragma unroll
-      for (int h = 0; h < G; ++h) {
-        float p = exp2f(a.logits[((int64_t)u * G + h) * row_stride + ridx] - sM[h]) * sIL[h];
-        a1 += p;
-        a2 += p * p;
-      }
-      float2* ap = isq ? &sm.acc_q[i - dsc.n_o - 1] : &sm.acc_o[i];
-      if (first) {
-        *ap = make_float2(a1, a2);
-      } else {
-        float2 c = *ap;
-        *ap = make_float2(c.x + a1, c.y + a2);
-      }
-    }
+  for (int h = 0; h < G; ++h) {
+    M[h] = a.mstat[((int64_t)u * G + h) * 2 + 0];
+    IL[h] = a.mstat[((int64_t)u * G + h) * 2 + 1];
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    UnitDesc nd = dsc;
-    nd.n_o = dsc.n_o + 1;
-    nd.t_next = dsc.t_next + 1;
-    a.desc[u] = nd;
+  const SlotMeta sm = slot_meta(a.meta, g, dsc.slot);
+  const int row_stride = g.cap_o + g.cap_q;
+  const bool isq = i >= dsc.n_o;
+  const int ridx = isq ? g.cap_o + (i - dsc.n_o) : i;
+  float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    const float p = exp2f(a.logits[((int64_t)u * G + h) * row_stride + ridx] - M[h]) * IL[h];
+    a1 += p;
+    a2 += p * p;
+  }
+  float2* ap = isq ? &sm.acc_q[i - dsc.n_o] : &sm.acc_o[i];
+  if (first) {
+    *ap = make_float2(a1, a2);
+  } else {
+    const float2 c = *ap;
+    *ap = make_float2(c.x + a1, c.y + a2);
+  }
+}
+
+void launch_decode_hh_acc(const DecodeArgs& a, int n_units_call, int max_rows, cudaStream_t s) {
+  dim3 grid((max_rows + 255) / 256, n_units_call);
+  switch (a.g.G) {
+    case 1: decode_hh_acc<1><<<grid, 256, 0, s>>>(a); break;
+    case 2: decode_hh_acc<2><<<grid, 256, 0, s>>>(a); break;
+    case 4: decode_hh_acc<4><<<grid, 256, 0, s>>>(a); break;
+    case 8: decode_hh_acc<8><<<grid, 256, 0, s>>>(a); break;
+    default: break;
   }
 }
 
@@ -340,8 +332,8 @@ void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s
 
 int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, const uint16_t* k, const uint16_t* v,
                   void* out, int out_fp32, uint8_t* slots, uint8_t* meta, UnitDesc* desc, float* partials,
-                  float* logits, int n_splits, int max_splits, int fast, int32_t* err, cudaStream_t s,
-                  cudaEvent_t ev0, cudaEvent_t ev1) {
+                  float* logits, float* mstat, int32_t* counters, int acc_rows, int n_splits, int max_splits,
+                  int fast, int32_t* err, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
   DecodeArgs a;
   a.g = g;
   a.layer0 = layer0;
@@ -356,19 +348,39 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
   a.desc = desc;
   a.partials = partials;
   a.logits = logits;
+  a.mstat = mstat;
+  a.counters = counters;
+  {
+    const char* e1 = std::getenv("ARKV_QGROUP");
+    const char* e2 = std::getenv("ARKV_INTERLEAVE");
+    a.q_group = e1 ? std::atoi(e1) : 0;           // default: as many Q tiles as fit a stage
+    a.interleave = e2 ? std::atoi(e2) : 0;        // measured: interleaving O/Q items is slower
+    const char* e3 = std::getenv("ARKV_FUSE_COMBINE");
+    a.fuse_combine = e3 ? std::atoi(e3) : 0;      // measured: the separate combine kernel is faster
+  }
   a.out = out;
   a.out_fp32 = out_fp32;
   a.err = err;
   const int n_units_call = g.batch * n_layers * g.Hkv;
-  if (fast) return launch_decode_fast(a, n_units_call, s, ev0, ev1);
-  switch (g.G) {
-    case 1: launch_g<1>(a, n_units_call, s, ev0, ev1); break;
-    case 2: launch_g<2>(a, n_units_call, s, ev0, ev1); break;
-    case 4: launch_g<4>(a, n_units_call, s, ev0, ev1); break;
-    case 8: launch_g<8>(a, n_units_call, s, ev0, ev1); break;
-    default: return -1;
+  int n = -1;
+  if (fast) {
+    n = launch_decode_fast(a, n_units_call, s, ev0, ev1);
+    if (n < 0) return n;
+  } else {
+    switch (g.G) {
+      case 1: launch_g<1>(a, n_units_call, s, ev0, ev1); break;
+      case 2: launch_g<2>(a, n_units_call, s, ev0, ev1); break;
+      case 4: launch_g<4>(a, n_units_call, s, ev0, ev1); break;
+      case 8: launch_g<8>(a, n_units_call, s, ev0, ev1); break;
+      default: return -1;
+    }
+    n = 2;
   }
-  return 2;
+  if (acc_rows > 0) {
+    launch_decode_hh_acc(a, n_units_call, acc_rows, s);
+    ++n;
+  }
+  return n;
 }
 
 }  // namespace arkv

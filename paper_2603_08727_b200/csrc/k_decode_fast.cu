@@ -21,7 +21,7 @@
 //  * HH accumulation (Eq. 9, R19): in the W steps before a tailor the logits are
 //    written out for the combine kernel; the new token (D1) is appended by the CTA
 //    owning the last Original tile and folded into its partial.
-#include "kernels.h"
+#include "combine.cuh"
 
 namespace arkv {
 
@@ -134,6 +134,8 @@ struct Smem {
   float wl[kConsumers][8];            // sum of p
   float wz[kConsumers][8][4];         // Σ p·z_v per head, per group
   float newtok[3][8];                 // new token: logit per head (log2), valid flag
+  float cM[8], cIL[8];                // fused combine: merged max and 1/sum per head
+  int is_last;                        // this CTA is the last split of its unit to finish
 };
 
 // Converts the fp32 P' block (thread holds rows gq, gq+8 x cols 2t, 2t+1) into the PV
@@ -199,7 +201,35 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) 
   const int S = a.n_splits, s = blockIdx.x;
   const int o0 = (int)((int64_t)s * tiles_o / S), o1 = (int)((int64_t)(s + 1) * tiles_o / S);
   const int q0 = (int)((int64_t)s * tiles_q / S), q1 = (int)((int64_t)(s + 1) * tiles_q / S);
-  const int n_work = (o1 - o0) + (q1 - q0);
+  // work items: single Original tiles and groups of up to q_per Quantized tiles (the
+  // Q stack grows down, so a group is one contiguous bulk copy), interleaved evenly so
+  // byte-heavy (O) and ALU-heavy (Q) items alternate across the consumer warps
+  const int q_per = a.q_group > 0 ? min(a.q_group, kStageBytes / g.tile_q) : kStageBytes / g.tile_q;
+  const int n_oi = o1 - o0, n_qi = (q1 - q0 + q_per - 1) / q_per;
+  const int n_work = n_oi + n_qi;
+  auto item_of = [&](int i, bool& isq, int& first, int& ntiles) {
+    int qb;
+    if (a.interleave) {
+      qb = (int)(((int64_t)i * n_qi) / max(n_work, 1));
+      isq = (int)(((int64_t)(i + 1) * n_qi) / max(n_work, 1)) > qb;
+    } else {  // all Original tiles first, then the Quantized groups
+      isq = i >= n_oi;
+      qb = isq ? i - n_oi : 0;
+      if (!isq) qb = 0;
+    }
+    if (!a.interleave && !isq) {
+      first = o0 + i;
+      ntiles = 1;
+      return;
+    }
+    if (isq) {
+      first = q0 + qb * q_per;
+      ntiles = min(q_per, q1 - first);
+    } else {
+      first = o0 + (i - qb);
+      ntiles = 1;
+    }
+  };
   const bool owns_new = (o0 <= n_o / kTile) && (n_o / kTile < o1);
   const int row_stride = g.cap_o + g.cap_q;
   const int64_t qkv = (int64_t)(b * a.n_layers + li);
@@ -224,9 +254,11 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) 
       for (int i = 0; i < n_work; ++i) {
         const int st = i % kStages;
         if (i >= kStages) mbar_wait(&sm.empty[st], ((i / kStages) - 1) & 1);
-        const bool isq = i >= (o1 - o0);
-        const uint8_t* src = isq ? q_tile_ptr(slot, g, q0 + (i - (o1 - o0))) : o_tile_ptr(slot, g, o0 + i);
-        const uint32_t bytes = isq ? (uint32_t)g.tile_q : (uint32_t)g.tile_o;
+        bool isq;
+        int first, ntiles;
+        item_of(i, isq, first, ntiles);
+        const uint8_t* src = isq ? q_tile_ptr(slot, g, first + ntiles - 1) : o_tile_ptr(slot, g, first);
+        const uint32_t bytes = isq ? (uint32_t)(ntiles * g.tile_q) : (uint32_t)g.tile_o;
         mbar_expect_tx(&sm.full[st], bytes);
         bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
       }
@@ -321,9 +353,12 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) 
       const int st = i % kStages;
       mbar_wait(&sm.full[st], (i / kStages) & 1);
       __syncwarp();  // lanes may leave the spin-wait in different iterations; mma/movmatrix are .aligned
-      const uint8_t* tb = sm.ring[st];
-      const bool isq = i >= (o1 - o0);
-      const int tile = isq ? q0 + (i - (o1 - o0)) : o0 + i;
+      bool isq;
+      int first, ntiles;
+      item_of(i, isq, first, ntiles);
+      for (int jt = 0; jt < ntiles; ++jt) {
+      const uint8_t* tb = sm.ring[st] + (isq ? (ntiles - 1 - jt) * g.tile_q : 0);
+      const int tile = first + jt;
       const int n_valid = isq ? min(kTile, n_q - tile * kTile) : min(kTile, n_o - tile * kTile);
 
       // ---- S = K q^T, logits in the log2 domain ----
@@ -513,6 +548,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) 
           }
         }
       }
+      }  // tiles of the item
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[st]);
     }
@@ -589,6 +625,20 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) 
       part[h * (D + 2) + 1] = L;
     }
   }
+  // ---- fused combine: the last split CTA of the unit to finish merges all partials ----
+  if (!a.fuse_combine) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(&a.counters[u], 1);
+    sm.is_last = prev == S - 1;
+  }
+  __syncthreads();
+  if (sm.is_last) {
+    __threadfence();
+    combine_unit<G>(a, u, b, li, kvh, dsc, sm.cM, sm.cIL);
+    if (threadIdx.x == 0) a.counters[u] = 0;
+  }
 }
 
 template <int G, int NG>
@@ -632,6 +682,7 @@ int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
     default: return -1;
   }
   if (r < 0) return -1;
+  if (a.fuse_combine) return 1;  // the last split CTA of each unit merged the partials
   launch_decode_combine(a, n_units_call, s);
   return 2;
 }

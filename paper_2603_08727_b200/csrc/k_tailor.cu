@@ -88,39 +88,56 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
     sh_prefix[threadIdx.x] = 0;
     sh_rem[threadIdx.x] = kk[threadIdx.x];
   }
-  uint64_t mask = 0;
-  for (int pass = 7; pass >= 0; --pass) {
+  __shared__ uint64_t sh_mask[2];
+  __shared__ int sh_done[2];
+  __shared__ uint32_t wsum[2][8];
+  if (threadIdx.x < 2) {
+    sh_mask[threadIdx.x] = 0;
+    sh_done[threadIdx.x] = kk[threadIdx.x] == 0;
+  }
+  __syncthreads();
+  for (int pass = 7; pass >= 0 && !(sh_done[0] && sh_done[1]); --pass) {
     for (int i = threadIdx.x; i < 512; i += blockDim.x) (&hist[0][0])[i] = 0;
+    const uint64_t p0 = sh_prefix[0], p1 = sh_prefix[1], m0 = sh_mask[0], m1 = sh_mask[1];
+    const bool d0 = sh_done[0], d1 = sh_done[1];
     __syncthreads();
-    const uint64_t p0 = sh_prefix[0], p1 = sh_prefix[1];
     const int sh = pass * 8;
     for (int i = threadIdx.x; i < n_e; i += blockDim.x) {
       float2 a;
       int p;
       rv.get(i, a, p);
-      uint64_t key = hh_key(a, p, invN, gamma);
-      uint32_t dg = (uint32_t)(key >> sh) & 0xFFu;
-      if ((key & mask) == p0) atomicAdd(&hist[0][dg], 1u);
-      if ((key & mask) == p1) atomicAdd(&hist[1][dg], 1u);
+      const uint64_t key = hh_key(a, p, invN, gamma);
+      const uint32_t dg = (uint32_t)(key >> sh) & 0xFFu;
+      if (!d0 && (key & m0) == p0) atomicAdd(&hist[0][dg], 1u);
+      if (!d1 && (key & m1) == p1) atomicAdd(&hist[1][dg], 1u);
     }
     __syncthreads();
-    if (threadIdx.x < 2) {
-      int s = threadIdx.x;
-      uint32_t rem = sh_rem[s];
-      if (rem > 0) {
-        uint32_t cum = 0;
-        for (int dgt = 255; dgt >= 0; --dgt) {
-          uint32_t h = hist[s][dgt];
-          if (cum + h >= rem) {
-            sh_prefix[s] |= ((uint64_t)dgt) << sh;
-            sh_rem[s] = rem - cum;
-            break;
-          }
-          cum += h;
-        }
+    // parallel digit search: threads [256 s, 256 s + 256) scan selection s's bins from
+    // the top digit down (inclusive prefix sums via warp shuffles)
+    const int sel = threadIdx.x >> 8, bi = threadIdx.x & 255, lw = (threadIdx.x >> 5) & 7, ln = threadIdx.x & 31;
+    uint32_t h = 0, incl = 0;
+    if (sel < 2) {
+      h = hist[sel][255 - bi];
+      incl = h;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (ln >= o) incl += v;
+      }
+      if (ln == 31) wsum[sel][lw] = incl;
+    }
+    __syncthreads();
+    if (sel < 2 && !(sel ? d1 : d0)) {
+      for (int w = 0; w < lw; ++w) incl += wsum[sel][w];
+      const uint32_t rem = sh_rem[sel], excl = incl - h;
+      if (h > 0 && excl < rem && rem <= incl) {
+        const int dgt = 255 - bi;
+        sh_prefix[sel] |= ((uint64_t)dgt) << sh;
+        sh_mask[sel] |= 0xFFull << sh;
+        if (rem - excl == h) sh_done[sel] = 1;  // the whole bucket is taken: threshold found
+        else sh_rem[sel] = rem - excl;
       }
     }
-    mask |= 0xFFull << sh;
     __syncthreads();
   }
   // thresholds: k-th largest key (k == 0 -> nothing selected)

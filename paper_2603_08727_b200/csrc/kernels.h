@@ -51,6 +51,11 @@ struct DecodeArgs {
   UnitDesc* desc;
   float* partials;
   float* logits;
+  float* mstat;  // [unit][G][2]: merged max (log2) and 1/sum of the step, for the HH kernel
+  int32_t* counters;  // [unit]: split CTAs finished this step (fused combine); reset by the last
+  int q_group;        // fast kernel: Quantized tiles per bulk copy (0 = as many as fit a stage)
+  int interleave;     // fast kernel: interleave Original and Quantized work items
+  int fuse_combine;   // fast kernel: the last split CTA of a unit merges the partials
   void* out;
   int out_fp32;
   int32_t* err;
@@ -59,8 +64,8 @@ struct DecodeArgs {
 // Decode attention (D1, D3, D7) for units [layer0, layer0+n) of all sequences.
 int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, const uint16_t* k, const uint16_t* v,
                   void* out, int out_fp32, uint8_t* slots, uint8_t* meta, UnitDesc* desc, float* partials,
-                  float* logits, int n_splits, int max_splits, int fast, int32_t* err, cudaStream_t s,
-                  cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+                  float* logits, float* mstat, int32_t* counters, int acc_rows, int n_splits, int max_splits,
+                  int fast, int32_t* err, cudaStream_t s, cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
 }  // namespace arkv
 
