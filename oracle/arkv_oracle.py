@@ -141,7 +141,9 @@ def key_mass(a_tilde: np.ndarray) -> np.ndarray:
 def compute_stats(p: np.ndarray, stat_eps: float = 1e-30) -> Tuple[float, float, float]:
     """Eq. 3 entropy (natural log, R2; 0 ln 0 = 0), Eq. 4 variance with p̄ = 1/n (R4,
     population divisor), Eq. 5 Pearson kurtosis m4/m2² (R5).  Degenerate cases (R6):
-    each statistic is clamped below at stat_eps, and 𝓚 := 1 when m2 <= stat_eps."""
+    each statistic is clamped below at stat_eps, and 𝓚 := 1 when m2 <= stat_eps.
+    Parity unpinned: the value of stat_eps (the paper is silent); the moments themselves
+    are pinned to closed forms and SPEC's printed values."""
     p = np.asarray(p, dtype=np.float64)
     n = p.shape[0]
     nz = p > 0
@@ -202,6 +204,8 @@ def tailor_counts(K: int, rho: float, cfg: Cfg) -> Tuple[int, int]:
     Eligible n_e = K − W; keep b = ⌊α n_e⌋; of the kept, n_oe Original
     (Top-B_o, capped so that the post-tailor usage leaves W tokens of headroom,
     R14) and n_q Quantized (the rest of the keep set, capped by bytes).
+    Parity unpinned: the headroom rule (R14) is this design's reading; the formula is
+    pinned to a brute-force byte walk of the same rule.
     Returns (n_oe, n_q): eligible tokens kept Original, tokens kept Quantized."""
     W, B = cfg.window, cfg.budget_tokens
     Co, Cq, Bb = cost_orig(cfg), cost_quant(cfg), budget_bytes(cfg)
@@ -220,7 +224,8 @@ def prefill_needs_tailor(P: int, cfg: Cfg) -> bool:
 
 def decode_needs_tailor(n_o: int, n_q: int, cfg: Cfg) -> bool:
     """R12: after the append, tailor iff the unit exceeds its budget, U > B_bytes
-    (Eq. 1 holds with ≤ at every attention step)."""
+    (Eq. 1 holds with ≤ at every attention step).  Parity unpinned: "reaches the limit"
+    (P:250) does not fix > versus >=."""
     return usage_bytes(cfg, n_o, n_q) > budget_bytes(cfg)
 
 
@@ -443,7 +448,8 @@ class UnitCache:
         """Eq. 10 tailor (Alg. 1) with the D6 transitions:
         O->Q quantize, Q->O promote (R24), Q->Q keep codes (R25), ->E drop.
         rows: list of (key positions [n], probs [r][n]) — the Eq. 2 window rows
-        (R19); every eligible token must appear in every row."""
+        (R19); every eligible token must appear in every row.  Parity unpinned: which
+        queries form the decode-time window (R19) is this design's reading.""" 
         cfg = self.cfg
         W = cfg.window
         K = self.n_o + self.n_q

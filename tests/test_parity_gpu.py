@@ -207,3 +207,40 @@ def test_determinism_bitwise():
     assert torch.equal(outs[0][0], outs[1][0])
     for key in ("state", "o_k", "q_k", "k_scale"):
         np.testing.assert_array_equal(outs[0][1][key], outs[1][1][key])
+
+
+def test_sharded_prefill_c1_equals_full():
+    """KV-head sharding: two caches holding KV heads [0,2) and [2,4) of the
+    same sequences; their Eq. 3 column sums are summed between arkv_prefill_begin and
+    arkv_prefill_finish (what NCCL all-reduce does across GPUs).  Statistics and rho
+    equal the unsharded cache bitwise; every unit's states, codes and outputs too."""
+    from paper_2603_08727_b200 import arkv as A
+    sh = Shape(batch=1, n_layers=2, n_q_heads=8, n_kv_heads=4, head_dim=128, prompt_len=1024, window=32)
+    qw, k, v = prefill_inputs(sh, seed=17)
+    mk = lambda hkv, hq: A.make_config(2, hq, hkv, 128, budget_tokens=256, max_positions=1024 + 40, max_prompt=1024)
+    full = A.ArkvCache(mk(4, 8))
+    st_f, oq_f, rho_f = full.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda())
+    halves = [A.ArkvCache(mk(2, 4)) for _ in range(2)]
+    parts = []
+    for i, c in enumerate(halves):
+        qwi = qw[:, :, 4 * i:4 * i + 4].contiguous().cuda()
+        ki, vi = k[:, :, 2 * i:2 * i + 2].contiguous().cuda(), v[:, :, 2 * i:2 * i + 2].contiguous().cuda()
+        parts.append((ki, vi, c.arkv_prefill_begin(qwi, ki)))
+    colsum = parts[0][2] + parts[1][2]
+    for i, c in enumerate(halves):
+        st, oq, rho = c.arkv_prefill_finish(parts[i][0], parts[i][1], colsum)
+        np.testing.assert_array_equal(rho, rho_f)
+        np.testing.assert_allclose(st.cpu().numpy(), st_f.cpu().numpy(), rtol=1e-12)
+    for s in range(40):
+        q, kn, vn = decode_inputs(sh, s, seed=17)
+        of = full.arkv_decode_step(q.cuda(), kn.cuda(), vn.cuda())
+        for i, c in enumerate(halves):
+            oh = c.arkv_decode_step(q[:, :, 4 * i:4 * i + 4].contiguous().cuda(), kn[:, :, 2 * i:2 * i + 2].contiguous().cuda(),
+                                    vn[:, :, 2 * i:2 * i + 2].contiguous().cuda())
+            torch.testing.assert_close(oh, of[:, :, 4 * i:4 * i + 4], rtol=0, atol=0)
+    for i, c in enumerate(halves):
+        for l in range(2):
+            for h in range(2):
+                e, r = c.arkv_export_unit(0, l, h), full.arkv_export_unit(0, l, 2 * i + h)
+                for key in ("state", "q_k", "k_scale", "o_v"):
+                    np.testing.assert_array_equal(e[key], r[key])
