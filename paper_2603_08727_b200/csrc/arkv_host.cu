@@ -568,7 +568,6 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<TailorJob> jobs;
   int max_tiles = 1, acc_rows = 0;
-  double max_bytes = 0.0;
   for (int b = 0; b < g.batch; ++b)
     for (int l = layer0; l < layer0 + n_layers; ++l) {
       const int bl = b * g.L + l;
@@ -601,7 +600,6 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
       }
       const int tiles = (c->n_o[bl] + 1 + kTile - 1) / kTile + (c->n_q[bl] + kTile - 1) / kTile;
       max_tiles = std::max(max_tiles, tiles);
-      max_bytes = std::max(max_bytes, (double)(c->n_o[bl] + 1) * g.cost_o + (double)c->n_q[bl] * g.cost_q);
       if (t >= c->trig[bl] - g.W && t < c->trig[bl])  // HH accumulation step (R19)
         acc_rows = std::max(acc_rows, c->n_o[bl] + 1 + c->n_q[bl]);
     }
@@ -609,22 +607,13 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
     arkv_status st = run_jobs(c, jobs, nullptr, nullptr, 0, s);
     if (st != ARKV_OK) return st;
   }
-  // split-K fan-out: minimise the wave-quantised time ceil(units*S/slots) * (1/S + f),
-  // f = per-CTA fixed cost relative to streaming a whole unit; never more splits than tiles
+  // split-K fan-out: ~2.6 waves of CTAs (measured at configs[1]: S = 3 beats 2 and 4; more
+  // splits cost pipeline fill/drain per CTA and combine reads), never more splits than tiles
   const int n_units_call = g.batch * n_layers * g.Hkv;
   const int slots = c->num_sms * (c->fast ? 2 : 4);
-  const double per_cta_bw = 5.0e12 / slots, t_fixed = 6.0e-6;  // measured sweep: S = 2..3 at configs[1]
-  const double f = t_fixed / std::max(max_bytes / per_cta_bw, 1e-9);
-  int S = 1;
-  double best = 1e300;
-  for (int cand = 1; cand <= std::min(c->max_splits, max_tiles); ++cand) {
-    const double waves = std::ceil((double)n_units_call * cand / slots);
-    const double cost = waves * (1.0 / cand + f);
-    if (cost < best - 1e-12) {
-      best = cost;
-      S = cand;
-    }
-  }  if (const char* env = std::getenv("ARKV_SPLITS")) {  // tuning knob (bench sweeps)
+  int S = (int)std::lround(2.6 * slots / (double)n_units_call);
+  S = std::max(1, std::min(S, std::min(c->max_splits, max_tiles)));
+  if (const char* env = std::getenv("ARKV_SPLITS")) {  // tuning knob (bench sweeps)
     const int v = std::atoi(env);
     if (v > 0) S = std::min(v, std::min(c->max_splits, max_tiles));
   }

@@ -321,15 +321,24 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) 
         qh[c][0] = pack_f16(f0, f4);
         qh[c][1] = pack_f16(f1 * 0.0625f, f5 * 0.0625f);
       }
+      // Σ_x q[h][x] per group: lane sums its 4 dims, segmented butterfly over the
+      // 32/NG lanes of each group, then the owner lanes pick their heads' sums
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int h = 2 * tq + e;
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int gr = 0; gr < NG; ++gr) qsum[e][gr] = 0.f;
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        float v = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v += bf16_to_f(qp[h * D + lane * 4 + i]);
+#pragma unroll
+        for (int off = 1; off < 32 / NG; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
 #pragma unroll
         for (int gr = 0; gr < NG; ++gr) {
-          float sacc = 0.f;
-          if (h < G)
-            for (int x = gr * (D / NG); x < (gr + 1) * (D / NG); ++x) sacc += bf16_to_f(qp[h * D + x]);
-          qsum[e][gr] = sacc;
+          const float sgr = __shfl_sync(0xffffffffu, v, gr * (32 / NG));
+          if (2 * tq == h) qsum[0][gr] = sgr;
+          if (2 * tq + 1 == h) qsum[1][gr] = sgr;
         }
       }
     }
