@@ -180,6 +180,12 @@ arkv_status arkv_check(arkv_cache* cache, void* stream);
 arkv_status arkv_schedule(const arkv_config* cfg, int32_t prompt_len, double rho, int32_t n_steps,
                           int32_t* events, int32_t max_events, int32_t* n_events);
 
+/* Host only.  Verifies the cache's tile layout: the Original-tile element
+   offsets are a bijection onto the tile's 2-byte cells, the Quantized-tile code bits plus
+   the fp32 scale/zero cells cover the tile exactly once, and the code-slot inverse used by
+   the tailor's packing pass inverts the forward map.  ARKV_ERR_DEVICE on a violation. */
+arkv_status arkv_layout_check(const arkv_config* cfg, int64_t* n_checked);
+
 /* Host only.  Statistics -> OQ score (Eq. 6 with the R6 clamps applied to the raw
    moments). */
 arkv_status arkv_oq_score(const arkv_config* cfg, double entropy, double m2, double m4, double* stats3,

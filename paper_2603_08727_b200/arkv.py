@@ -47,7 +47,7 @@ EXPORTED = [
     "arkv_prefill_stats", "arkv_decode_step", "arkv_unit_counts", "arkv_export_unit",
     "arkv_check", "arkv_schedule", "arkv_oq_score", "arkv_launch_count", "arkv_version",
     "arkv_status_string", "arkv_cache_info", "arkv_prefill_begin", "arkv_prefill_finish",
-    "arkv_profile", "arkv_profile_read",
+    "arkv_profile", "arkv_profile_read", "arkv_layout_check",
 ]
 
 _lib = None
@@ -72,6 +72,7 @@ def lib() -> ctypes.CDLL:
         L.arkv_check.argtypes = [vp, vp]
         L.arkv_schedule.argtypes = [P(ArkvConfig), i32, dbl, i32, P(i32), i32, P(i32)]
         L.arkv_oq_score.argtypes = [P(ArkvConfig), dbl, dbl, dbl, P(dbl), P(dbl)]
+        L.arkv_layout_check.argtypes = [P(ArkvConfig), P(ctypes.c_int64)]
         L.arkv_cache_info.argtypes = [vp, i32]
         L.arkv_cache_info.restype = ctypes.c_int32
         L.arkv_prefill_begin.argtypes = [vp, vp, vp, i32, vp, vp]
@@ -130,6 +131,12 @@ def arkv_schedule(cfg: ArkvConfig, prompt_len: int, rho: float, n_steps: int, ma
     _ok(lib().arkv_schedule(ctypes.byref(cfg), prompt_len, rho, n_steps, ev, max_events, ctypes.byref(n)),
         "arkv_schedule")
     return [tuple(ev[4 * i:4 * i + 4]) for i in range(min(n.value, max_events))]
+
+
+def arkv_layout_check(cfg: ArkvConfig) -> int:
+    n = ctypes.c_int64()
+    _ok(lib().arkv_layout_check(ctypes.byref(cfg), ctypes.byref(n)), "arkv_layout_check")
+    return n.value
 
 
 def arkv_oq_score(cfg: ArkvConfig, entropy: float, m2: float, m4: float):

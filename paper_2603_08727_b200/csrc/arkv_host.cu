@@ -291,6 +291,61 @@ arkv_status arkv_schedule(const arkv_config* cfg, int32_t P, double rho, int32_t
   return ARKV_OK;
 }
 
+arkv_status arkv_layout_check(const arkv_config* cfg, int64_t* n_checked) {
+  arkv_status st = validate(cfg);
+  if (st != ARKV_OK) return st;
+  const Geom g = compute_sizes(*cfg).g;
+  int64_t n = 0;
+  // Original tile: every (token, dim) of K and V maps to a distinct 2-byte cell; all cells used
+  std::vector<uint8_t> seen(g.tile_o, 0);
+  for (int j = 0; j < kTile; ++j)
+    for (int x = 0; x < g.d; ++x)
+      for (int v = 0; v < 2; ++v) {
+        const int off = v ? o_v_off(g, j, x) : o_k_off(g, j, x);
+        if (off < 0 || off + 2 > g.tile_o || (off & 1) || seen[off] || seen[off + 1]) return ARKV_ERR_DEVICE;
+        seen[off] = seen[off + 1] = 1;
+        ++n;
+      }
+  for (uint8_t b : seen)
+    if (!b) return ARKV_ERR_DEVICE;
+  // Quantized tile: codes (bit level) and scales/zeros cover the tile exactly once, and
+  // q_code_slot inverts q_k_loc / q_v_loc
+  std::vector<uint8_t> bits((size_t)g.tile_q * 8, 0);
+  for (int j = 0; j < kTile; ++j)
+    for (int x = 0; x < g.d; ++x)
+      for (int v = 0; v < 2; ++v) {
+        int byte, shift;
+        if (v) q_v_loc(g, j, x, &byte, &shift);
+        else q_k_loc(g, j, x, &byte, &shift);
+        if (byte < 0 || byte >= g.tile_q || shift % g.bits) return ARKV_ERR_DEVICE;
+        for (int b = 0; b < g.bits; ++b) {
+          if (bits[(size_t)byte * 8 + shift + b]) return ARKV_ERR_DEVICE;
+          bits[(size_t)byte * 8 + shift + b] = 1;
+        }
+        int jj, xx, vv;
+        if (!q_code_slot(g, byte, shift / g.bits, &jj, &xx, &vv) || jj != j || xx != x || vv != v)
+          return ARKV_ERR_DEVICE;
+        ++n;
+      }
+  for (int j = 0; j < kTile; ++j)
+    for (int w = 0; w < 4; ++w)
+      for (int gr = 0; gr < g.ng; ++gr) {
+        const int off = q_sc_off(g, j, w, gr);
+        if (off < 0 || off + 4 > g.tile_q || (off & 3)) return ARKV_ERR_DEVICE;
+        for (int b = 0; b < 32; ++b) {
+          if (bits[(size_t)off * 8 + b]) return ARKV_ERR_DEVICE;
+          bits[(size_t)off * 8 + b] = 1;
+        }
+        int jj, xx, vv;
+        if (q_code_slot(g, off, 0, &jj, &xx, &vv)) return ARKV_ERR_DEVICE;
+        ++n;
+      }
+  for (uint8_t b : bits)
+    if (!b) return ARKV_ERR_DEVICE;
+  if (n_checked) *n_checked = n;
+  return ARKV_OK;
+}
+
 arkv_status arkv_oq_score(const arkv_config* cfg, double H, double m2, double m4, double* stats3, double* score) {
   if (!cfg) return ARKV_ERR_INVALID_ARG;
   const double eps = cfg->stat_eps;

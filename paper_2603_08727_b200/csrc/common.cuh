@@ -150,6 +150,40 @@ __host__ __device__ inline int q_sc_off(const Geom& g, int j, int which, int grp
   return 32 * g.d + ((which * g.ng + grp) * 32 + j) * 4;
 }
 
+// Inverse of q_k_loc / q_v_loc: the code held by slot s (s < 8/bits, at bit s*bits) of
+// byte B of a Quantized tile.  Returns false for scale/zero bytes.
+__host__ __device__ inline bool q_code_slot(const Geom& g, int B, int s, int* j, int* x, int* isv) {
+  if (g.layout != ARKV_LAYOUT_FRAG) {
+    const int per = 8 / g.bits, cb = g.d * g.bits / 8;
+    const int row = B / g.cost_q, off = B % g.cost_q;
+    if (off >= 2 * cb) return false;
+    *j = row;
+    *isv = off >= cb;
+    *x = (*isv ? off - cb : off) * per + s;
+    return true;
+  }
+  if (B >= 32 * g.d) return false;
+  const bool v = B >= 16 * g.d;
+  const int bl = v ? B - 16 * g.d : B;
+  const int w = bl >> 2, bw = bl & 3;
+  const int lane = (w >> 2) & 31, k = ((w >> 7) << 2) | (w & 3);
+  const int gg = lane >> 2, t = lane & 3;
+  const int e = 2 * bw + s;
+  if (!v) {
+    const int nq = g.d >> 5;
+    const int mth = k / nq, jp = k % nq;
+    *j = (mth >> 1) * 16 + (mth & 1) * 8 + gg;
+    *x = 32 * jp + 8 * t + e;
+    *isv = 0;
+  } else {
+    const int mtv = k >> 1, sel = k & 1;
+    *x = 16 * mtv + 8 * sel + gg;
+    *j = 16 * ((e >> 1) & 1) + 8 * (e & 1) + 2 * t + (e >> 2);
+    *isv = 1;
+  }
+  return true;
+}
+
 __device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 __device__ __forceinline__ uint16_t f_to_bf16_rne(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));

@@ -274,13 +274,24 @@ __device__ __forceinline__ uint32_t read_code(const Geom& g, const uint8_t* tile
   return (w >> shift) & ((1u << g.bits) - 1u);
 }
 
-__device__ __forceinline__ void write_code(const Geom& g, uint8_t* tile, int j, int x, bool isv, uint32_t c) {
-  int byte, shift;
-  if (isv) q_v_loc(g, j, x, &byte, &shift);
-  else q_k_loc(g, j, x, &byte, &shift);
-  // codes of different dims/tokens may share a 32-bit word: OR into the zeroed tile
-  uint32_t* wp = (uint32_t*)(tile + (byte & ~3));
-  atomicOr(wp, c << (shift + 8 * (byte & 3)));
+// Codes are first collected one per byte in cbuf[isv][token][dim] (shared memory), then
+// packed into the tile layout by pack_codes (no read-modify-write on shared words).
+__device__ __forceinline__ void write_code(const Geom& g, uint8_t* cbuf, int j, int x, bool isv, uint32_t c) {
+  cbuf[((isv ? kTile : 0) + j) * g.d + x] = (uint8_t)c;
+}
+
+__device__ __forceinline__ void pack_codes(const Geom& g, uint8_t* tile, const uint8_t* cbuf, int tbytes) {
+  const int per = 8 / g.bits;
+  for (int B = threadIdx.x; B < tbytes; B += blockDim.x) {
+    int j, x, isv;
+    if (!q_code_slot(g, B, 0, &j, &x, &isv)) continue;  // scale / zero bytes
+    uint32_t v = 0;
+    for (int s = 0; s < per; ++s) {
+      q_code_slot(g, B, s, &j, &x, &isv);
+      v |= (uint32_t)cbuf[((isv ? kTile : 0) + j) * g.d + x] << (s * g.bits);
+    }
+    tile[B] = (uint8_t)v;
+  }
 }
 
 __device__ __forceinline__ float read_o(const Geom& g, const uint8_t* tile, int j, int x, bool isv) {
@@ -303,7 +314,9 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g, TailorJobs job
   const bool dstQ = tid >= tiles_o;
   if (dstQ) tid -= tiles_o;
   const int tbytes = dstQ ? g.tile_q : g.tile_o;
-  for (int i = threadIdx.x * 4; i < tbytes; i += blockDim.x * 4) *(uint32_t*)(tile + i) = 0u;
+  uint8_t* cbuf = tile + ((tbytes + 15) & ~15);  // [2][32][d] code bytes (Quantized tiles)
+  const int zbytes = dstQ ? ((tbytes + 15) & ~15) + 2 * kTile * g.d : tbytes;
+  for (int i = threadIdx.x * 4; i < zbytes; i += blockDim.x * 4) *(uint32_t*)(tile + i) = 0u;
   __syncthreads();
 
   const int32_t* src = src_scratch + (int64_t)blockIdx.y * src_stride + (dstQ ? g.cap_o : 0);
@@ -346,8 +359,8 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g, TailorJobs job
     if (kind == kSrcOldQ && dstQ) {
       // Q -> Q: copy codes and scales (R25)
       for (int x = lane; x < g.d; x += 32) {
-        write_code(g, tile, j, x, false, read_code(g, qt, oj, x, false));
-        write_code(g, tile, j, x, true, read_code(g, qt, oj, x, true));
+        write_code(g, cbuf, j, x, false, read_code(g, qt, oj, x, false));
+        write_code(g, cbuf, j, x, true, read_code(g, qt, oj, x, true));
       }
       for (int w = lane; w < 4 * g.ng; w += 32) {
         int which = w / g.ng, grp = w % g.ng;
@@ -439,7 +452,7 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g, TailorJobs job
               c = __float2int_rn(__fdiv_rn(__fsub_rn(kvv[kv][t], mn), s));
               c = max(0, min((1 << g.bits) - 1, c));
             }
-            write_code(g, tile, j, x, kv == 1, (uint32_t)(c + off));
+            write_code(g, cbuf, j, x, kv == 1, (uint32_t)(c + off));
           }
         }
         if (lane == 0) {
@@ -450,6 +463,10 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g, TailorJobs job
     }
   }
   __syncthreads();
+  if (dstQ) {
+    pack_codes(g, tile, cbuf, tbytes);
+    __syncthreads();
+  }
   uint8_t* dst = dstQ ? q_tile_ptr(nslot, g, tid) : o_tile_ptr(nslot, g, tid);
   for (int i = threadIdx.x * 16; i < tbytes; i += blockDim.x * 16) *(uint4*)(dst + i) = *(const uint4*)(tile + i);
 }
@@ -461,7 +478,7 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
   const int src_stride = g.cap_o + g.cap_q;
   tailor_select_kernel<<<n_jobs, 1024, 0, s>>>(g, jobs, meta, acc_pf, st_scratch, st_stride);
   tailor_scan_kernel<<<n_jobs, 1024, 0, s>>>(g, jobs, desc, st_scratch, st_stride, src_scratch, src_stride, err);
-  size_t smem = (size_t)max(g.tile_o, g.tile_q);
+  size_t smem = (size_t)max(g.tile_o, ((g.tile_q + 15) & ~15) + 2 * kTile * g.d);
   dim3 grid(max_tiles, n_jobs);
   const int vpl = (g.d + 31) / 32;
 #define MV_CASE(V)                                                                                                \

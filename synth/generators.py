@@ -193,3 +193,49 @@ def prefill_inputs_fast(sh: Shape, seed: int = 0, device="cpu"):
             qq = beta[l] * u[l].repeat_interleave(G, dim=0)[:, None, :] + torch.randn(Hq, W, d, generator=g, device=device)
             qw[b, l] = qq.to(torch.bfloat16)
     return qw, k, v
+
+
+def prefill_inputs_margin_fast(sh: Shape, seed: int = 0, device="cpu"):
+    """Vectorised margin recipe (see module docstring) for full-size parity runs:
+    keys = level * u / sqrt(d) + 0.02 N with levels a shuffled arithmetic progression per
+    (sequence, layer, KV head) and ~3 % of keys bitwise copies of their predecessor."""
+    B, L, Hq, Hkv, d, P, W = (sh.batch, sh.n_layers, sh.n_q_heads, sh.n_kv_heads, sh.head_dim,
+                              sh.prompt_len, sh.window)
+    G = Hq // Hkv
+    u = _directions(sh, seed, device)
+    qw = torch.empty(B, L, Hq, W, d, dtype=torch.bfloat16, device=device)
+    k = torch.empty(B, L, Hkv, P, d, dtype=torch.bfloat16, device=device)
+    v = torch.empty(B, L, Hkv, P, d, dtype=torch.bfloat16, device=device)
+    idx = torch.arange(P, device=device)
+    lin = torch.linspace(0.0, 1.0, P, device=device)
+    for b in range(B):
+        for l in range(L):
+            g = _gen(seed, 6, b, l, device=device)
+            for h in range(Hkv):
+                lev = lin[torch.randperm(P, generator=g, device=device)]
+                kk = lev[:, None] * u[l, h][None, :] / math.sqrt(d) + 0.02 * torch.randn(P, d, generator=g, device=device)
+                dup = torch.rand(P, generator=g, device=device) < 0.03
+                src = torch.where(dup & (idx > 0), idx - 1, idx)
+                k[b, l, h] = kk[src].to(torch.bfloat16)
+            vv = torch.randn(Hkv, P, d, generator=g, device=device)
+            vv[..., :2] *= 8.0
+            v[b, l] = vv.to(torch.bfloat16)
+            amp = 0.6 + 0.4 * torch.rand(Hq, W, 1, generator=g, device=device)
+            qq = amp * u[l].repeat_interleave(G, dim=0)[:, None, :] * 4.0 + 0.02 * torch.randn(Hq, W, d, generator=g, device=device)
+            qw[b, l] = qq.to(torch.bfloat16)
+    return qw, k, v
+
+
+def decode_inputs_margin_fast(sh: Shape, step: int, seed: int = 0, device="cpu"):
+    """Vectorised margin-recipe decode inputs (new key at a random level along u)."""
+    B, L, Hq, Hkv, d = sh.batch, sh.n_layers, sh.n_q_heads, sh.n_kv_heads, sh.head_dim
+    G = Hq // Hkv
+    u = _directions(sh, seed, device)
+    g = _gen(seed, 8, step, device=device)
+    lev = torch.rand(B, L, Hkv, 1, generator=g, device=device)
+    k = lev * u[None] / math.sqrt(d) + 0.02 * torch.randn(B, L, Hkv, d, generator=g, device=device)
+    amp = 0.6 + 0.4 * torch.rand(B, L, Hq, 1, generator=g, device=device)
+    q = amp * u.repeat_interleave(G, dim=1)[None] * 4.0 + 0.02 * torch.randn(B, L, Hq, d, generator=g, device=device)
+    v = torch.randn(B, L, Hkv, d, generator=g, device=device)
+    v[..., :2] *= 8.0
+    return q.to(torch.bfloat16), k.to(torch.bfloat16), v.to(torch.bfloat16)

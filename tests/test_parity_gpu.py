@@ -244,3 +244,63 @@ def test_sharded_prefill_c1_equals_full():
                 e, r = c.arkv_export_unit(0, l, h), full.arkv_export_unit(0, l, 2 * i + h)
                 for key in ("state", "q_k", "k_scale", "o_v"):
                     np.testing.assert_array_equal(e[key], r[key])
+
+
+def test_full_size_configs1_sampled_units():
+    """configs[1] at full size, launched exactly as bench.py does (32 layers x 8 KV heads
+    in one arkv_decode_step per step, default kernel and split count): the oracle
+    recomputes sampled units one by one (two layers with different rho, two KV heads
+    each) through the prefill-end tailor, the HH window and the first decode tailor."""
+    from paper_2603_08727_b200 import arkv as A
+    from synth import prefill_inputs_margin_fast, decode_inputs_margin_fast
+    sh = Shape(batch=1, n_layers=32, n_q_heads=32, n_kv_heads=8, head_dim=128, prompt_len=32768, window=32)
+    steps = 40
+    cfg = A.make_config(32, 32, 8, 128, budget_tokens=8192, max_positions=32768 + steps + 1, max_prompt=32768)
+    gpu = A.ArkvCache(cfg)
+    qw, k, v = prefill_inputs_margin_fast(sh, seed=23, device="cuda")
+    stats, oq, rho = gpu.arkv_prefill_stats(qw, k, v)
+    gpu.arkv_check()
+    order = np.argsort(rho[0])
+    layers = [int(order[0]), int(order[len(order) // 2])]       # most quantised + median layer
+    ocfg = O.Cfg(n_layers=1, n_q_heads=32, n_kv_heads=8, head_dim=128, window=32, budget_tokens=8192)
+    oras = {}
+    for l in layers:
+        ora = O.OracleARKV(ocfg)
+        sub = lambda t: t[:, l:l + 1].double().cpu().numpy()   # noqa: E731
+        ora.prefill(sub(qw), sub(k), sub(v), rho_override=[[rho[0, l]]])
+        oras[l] = ora
+    del qw, k, v
+    for l in layers:
+        for h in range(8):
+            e, r = gpu.arkv_export_unit(0, l, h), oras[l].export(0, 0, h)
+            assert (e["n_o"], e["n_q"]) == (r["n_o"], r["n_q"])
+            if min(oras[l].units[(0, 0, h)].margins) <= MARGIN:
+                continue
+            np.testing.assert_array_equal(e["state"], r["state"])
+            qm = r["state"] == 2
+            np.testing.assert_array_equal(e["q_k"][qm], r["q_k"][qm])
+            np.testing.assert_array_equal(e["v_scale"][qm], r["v_scale"][qm])
+    for s in range(steps):
+        q, kn, vn = decode_inputs_margin_fast(sh, s, seed=23, device="cuda")
+        out = gpu.arkv_decode_step(q, kn, vn, out_fp32=True).cpu().numpy()
+        for l in layers:
+            ref = oras[l].decode_step(q[:, l:l + 1].double().cpu().numpy(), kn[:, l:l + 1].double().cpu().numpy(),
+                                      vn[:, l:l + 1].double().cpu().numpy())
+            np.testing.assert_allclose(out[:, l:l + 1], ref, rtol=RTOL, atol=ATOL, err_msg=f"layer {l} step {s}")
+    gpu.arkv_check()
+    for l in layers:
+        assert len(oras[l].units[(0, 0, 0)].tailors) >= 2       # prefill-end + first decode tailor
+        full = 0
+        for h in range(8):
+            e, r = gpu.arkv_export_unit(0, l, h), oras[l].export(0, 0, h)
+            assert (e["n_o"], e["n_q"]) == (r["n_o"], r["n_q"])
+            margins = oras[l].units[(0, 0, h)].margins
+            if min(margins) <= MARGIN:
+                continue      # a near-tie at a rank threshold: fp32 vs fp64 may rank it differently
+            full += 1
+            np.testing.assert_array_equal(e["state"], r["state"])
+            om, qm = r["state"] == 1, r["state"] == 2
+            np.testing.assert_array_equal(_bf16_bits_to_f64(e["o_v"])[om], r["o_v"][om])
+            np.testing.assert_array_equal(e["q_k"][qm], r["q_k"][qm])
+            np.testing.assert_array_equal(e["k_zero"][qm], r["k_zero"][qm])
+        assert full >= 2, f"layer {l}: fewer than two units with a score margin"
