@@ -264,7 +264,8 @@ def run_arkv(args, wl):
         e2e = {"value": ws * B * n_e2e / (e2e_ms / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in hq[0])),
                "d2h_bytes_per_step": int(hout[0].numel() * hout[0].element_size()),
-               "pipeline": "H2D of step s+1 and D2H of step s overlap step s's compute (two copy streams)"}
+               "pipeline": "H2D of step s+1 and D2H of step s overlap step s's compute (two copy streams)",
+               "window": f"{n_e2e} decode steps following the device-timed window"}
     if ws > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -427,12 +428,14 @@ def main():
     ap.add_argument("--impl", default="arkv", choices=["arkv", "reference"])
     ap.add_argument("--workload", default="llama3-8b-32k", choices=sorted(WORKLOADS))
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 generic, 2 fast")
-    ap.add_argument("--e2e-steps", type=int, default=256)
+    ap.add_argument("--e2e-steps", type=int, default=-1, help="-1: same as --steps")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prompt-len", type=int, default=0, help="debug: override the workload's prompt length")
     ap.add_argument("--layers", type=int, default=0, help="debug: override the workload's layer count")
     args = ap.parse_args()
+    if args.e2e_steps < 0:
+        args.e2e_steps = args.steps
     wl = dict(WORKLOADS[args.workload])
     if args.prompt_len:
         wl["prompt_len"] = args.prompt_len

@@ -184,6 +184,12 @@ __host__ __device__ inline bool q_code_slot(const Geom& g, int B, int s, int* j,
   return true;
 }
 
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialization may start while its predecessor drains; it must wait before touching
+// memory the predecessor writes.  Both are no-ops for ordinary launches.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 __device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 __device__ __forceinline__ uint16_t f_to_bf16_rne(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));

@@ -40,6 +40,7 @@ __device__ __forceinline__ void bf16x8_to_f(uint4 w, float (&f)[8]) {
 template <int G, int LG>
 __global__ void __launch_bounds__(128) decode_split_generic(DecodeArgs a) {
   constexpr int TPP = 32 / LG;  // tokens per warp pass
+  griddep_wait();
   const Geom& g = a.g;
   const int d = g.d;
   int b, li, kvh, u;
@@ -233,6 +234,8 @@ __global__ void __launch_bounds__(128) decode_split_generic(DecodeArgs a) {
 // Combine: merge split partials, write the output, HH accumulation, advance the unit.
 template <int G>
 __global__ void __launch_bounds__(256) decode_combine(DecodeArgs a) {
+  griddep_wait();
+  griddep_launch_dependents();
   int b, li, kvh, u;
   unit_of(a, blockIdx.x, b, li, kvh, u);
   const UnitDesc dsc = a.desc[u];
@@ -246,6 +249,7 @@ __global__ void __launch_bounds__(256) decode_combine(DecodeArgs a) {
 // (the descriptor already counts the appended token); one thread per row.
 template <int G>
 __global__ void __launch_bounds__(256) decode_hh_acc(DecodeArgs a) {
+  griddep_wait();
   const Geom& g = a.g;
   int b, li, kvh, u;
   unit_of(a, blockIdx.y, b, li, kvh, u);
@@ -285,10 +289,10 @@ __global__ void __launch_bounds__(256) decode_hh_acc(DecodeArgs a) {
 void launch_decode_hh_acc(const DecodeArgs& a, int n_units_call, int max_rows, cudaStream_t s) {
   dim3 grid((max_rows + 255) / 256, n_units_call);
   switch (a.g.G) {
-    case 1: decode_hh_acc<1><<<grid, 256, 0, s>>>(a); break;
-    case 2: decode_hh_acc<2><<<grid, 256, 0, s>>>(a); break;
-    case 4: decode_hh_acc<4><<<grid, 256, 0, s>>>(a); break;
-    case 8: decode_hh_acc<8><<<grid, 256, 0, s>>>(a); break;
+    case 1: launch_pdl(decode_hh_acc<1>, grid, dim3(256), 0, s, a); break;
+    case 2: launch_pdl(decode_hh_acc<2>, grid, dim3(256), 0, s, a); break;
+    case 4: launch_pdl(decode_hh_acc<4>, grid, dim3(256), 0, s, a); break;
+    case 8: launch_pdl(decode_hh_acc<8>, grid, dim3(256), 0, s, a); break;
     default: break;
   }
 }
@@ -305,7 +309,7 @@ static void launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cuda
   switch (a.g.d / 8) {
 #define LG_CASE(LGV) \
   case LGV:          \
-    decode_split_generic<G, LGV><<<grid, 128, smem, s>>>(a); \
+    launch_pdl(decode_split_generic<G, LGV>, grid, dim3(128), smem, s, a); \
     break;
     LG_CASE(2)
     LG_CASE(4)
@@ -317,15 +321,15 @@ static void launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cuda
       break;
   }
   if (ev1) cudaEventRecord(ev1, s);
-  decode_combine<G><<<n_units_call, 256, 0, s>>>(a);
+  launch_pdl(decode_combine<G>, dim3(n_units_call), dim3(256), 0, s, a);
 }
 
 void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s) {
   switch (a.g.G) {
-    case 1: decode_combine<1><<<n_units_call, 256, 0, s>>>(a); break;
-    case 2: decode_combine<2><<<n_units_call, 256, 0, s>>>(a); break;
-    case 4: decode_combine<4><<<n_units_call, 256, 0, s>>>(a); break;
-    case 8: decode_combine<8><<<n_units_call, 256, 0, s>>>(a); break;
+    case 1: launch_pdl(decode_combine<1>, dim3(n_units_call), dim3(256), 0, s, a); break;
+    case 2: launch_pdl(decode_combine<2>, dim3(n_units_call), dim3(256), 0, s, a); break;
+    case 4: launch_pdl(decode_combine<4>, dim3(n_units_call), dim3(256), 0, s, a); break;
+    case 8: launch_pdl(decode_combine<8>, dim3(n_units_call), dim3(256), 0, s, a); break;
     default: break;
   }
 }
@@ -357,6 +361,8 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
     a.interleave = e2 ? std::atoi(e2) : 0;        // measured: interleaving O/Q items is slower
     const char* e3 = std::getenv("ARKV_FUSE_COMBINE");
     a.fuse_combine = e3 ? std::atoi(e3) : 0;      // measured: the separate combine kernel is faster
+    const char* e4 = std::getenv("ARKV_PRODUCER");
+    a.producer_mode = e4 ? std::atoi(e4) : 0;  // measured: in-order refill beats polling
   }
   a.out = out;
   a.out_fp32 = out_fp32;

@@ -21,6 +21,8 @@
 //  * HH accumulation (Eq. 9, R19): in the W steps before a tailor the logits are
 //    written out for the combine kernel; the new token (D1) is appended by the CTA
 //    owning the last Original tile and folded into its partial.
+#include <cstdlib>
+
 #include "combine.cuh"
 
 namespace arkv {
@@ -28,14 +30,12 @@ namespace arkv {
 namespace fast {
 
 constexpr int D = 128;
-constexpr int kConsumers = 4;
-// One ring stage per consumer warp (tile i -> warp i % 4 -> stage i % 4): every stage's
-// mbarriers are then waited on strictly in phase order by a single warp.  (With more
-// stages than warps a fast warp could wait on a stage two phases ahead, where
-// try_wait.parity reports the preceding phase as complete.)  64 KB ring: 2 CTAs/SM.
-constexpr int kStages = kConsumers;
+// C consumer warps, each owning SPW ring stages: item i -> warp i % C -> stage
+// (i % C) + C * ((i / C) % SPW).  Every stage's mbarriers are thus waited on strictly in
+// phase order by a single warp.  (A stage shared round-robin by several warps lets a
+// fast warp wait two phases ahead, where try_wait.parity reports the preceding phase as
+// complete — a real bug hit with 6 stages / 4 warps.)
 constexpr int kStageBytes = 32 * 4 * D;  // one Original tile (16 KB) — the largest
-constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ---- PTX helpers ------------------------------------------------------------------
@@ -59,6 +59,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -126,13 +137,15 @@ __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(_
 __device__ __forceinline__ float f16_round(float x) { return __half2float(__float2half_rn(x)); }
 __device__ __forceinline__ uint32_t word(const uint4& q, int i) { return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w; }
 
+template <int C, int SPW>
 struct Smem {
+  static constexpr int kStages = C * SPW;
   uint8_t ring[kStages][kStageBytes];
   uint64_t full[kStages];
   uint64_t empty[kStages];
-  float wm[kConsumers][8];            // per warp, per head: running max (log2 domain)
-  float wl[kConsumers][8];            // sum of p
-  float wz[kConsumers][8][4];         // Σ p·z_v per head, per group
+  float wm[C][8];                     // per warp, per head: running max (log2 domain)
+  float wl[C][8];                     // sum of p
+  float wz[C][8][4];                  // Σ p·z_v per head, per group
   float newtok[3][8];                 // new token: logit per head (log2), valid flag
   float cM[8], cIL[8];                // fused combine: merged max and 1/sum per head
   int is_last;                        // this CTA is the last split of its unit to finish
@@ -178,11 +191,17 @@ __device__ __forceinline__ void make_b(const float (&v)[4], int t, uint32_t& b01
   c01 = c23 = 0u;
 }
 
-template <int G, int NG>
-__global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) {
+template <int G, int NG, int C, int SPW>
+__global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536) ? 2 : 1)
+    decode_fast_kernel(DecodeArgs a) {
+  constexpr int kConsumers = C;
+  constexpr int kStages = C * SPW;
+  auto stage_of = [](int i) { return (i % C) + C * ((i / C) % SPW); };
+  auto phase_of = [](int i) { return (i / C) / SPW; };
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  Smem<C, SPW>& sm = *reinterpret_cast<Smem<C, SPW>*>(smem_raw);
   const Geom& g = a.g;
+  griddep_wait();  // PDL: the previous kernel (tailor / combine) has completed
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
 
@@ -251,9 +270,11 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) 
   if (warp == kConsumers) {
     // ===================== producer =====================
     if (lane == 0) {
+      // items in order (measured: polling stages out of order and busy-waiting costs the
+      // co-scheduled consumer warp issue slots; try_wait suspends in hardware)
       for (int i = 0; i < n_work; ++i) {
-        const int st = i % kStages;
-        if (i >= kStages) mbar_wait(&sm.empty[st], ((i / kStages) - 1) & 1);
+        const int st = stage_of(i);
+        if (i >= kStages) mbar_wait(&sm.empty[st], (phase_of(i) - 1) & 1);
         bool isq;
         int first, ntiles;
         item_of(i, isq, first, ntiles);
@@ -262,6 +283,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) 
         mbar_expect_tx(&sm.full[st], bytes);
         bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
       }
+      griddep_launch_dependents();  // PDL: the combine may start launching (it waits for us)
     }
     __syncwarp();  // reconverge before warp-collective code and the aligned CTA barrier
     // the producer warp also appends the step's token (D1) when this CTA owns its tile
@@ -359,8 +381,8 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) 
     const int src_lane = (lane & ~3) | src_t;
 
     for (int i = warp; i < n_work; i += kConsumers) {
-      const int st = i % kStages;
-      mbar_wait(&sm.full[st], (i / kStages) & 1);
+      const int st = stage_of(i);
+      mbar_wait(&sm.full[st], phase_of(i) & 1);
       __syncwarp();  // lanes may leave the spin-wait in different iterations; mma/movmatrix are .aligned
       bool isq;
       int first, ntiles;
@@ -650,15 +672,34 @@ __global__ void __launch_bounds__(kThreads, 2) decode_fast_kernel(DecodeArgs a) 
   }
 }
 
-template <int G, int NG>
-static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
-  auto kern = decode_fast_kernel<G, NG>;
-  const int smem = (int)sizeof(Smem);
+template <int G, int NG, int C, int SPW>
+static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+  auto kern = decode_fast_kernel<G, NG, C, SPW>;
+  const int smem = (int)sizeof(Smem<C, SPW>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   dim3 grid(a.n_splits, n_units_call);
   if (ev0) cudaEventRecord(ev0, s);
-  kern<<<grid, kThreads, smem, s>>>(a);
+  launch_pdl(kern, grid, dim3((C + 1) * 32), (size_t)smem, s, a);
   if (ev1) cudaEventRecord(ev1, s);
+}
+
+// Default pipeline shape: 4 consumer warps x 1 stage (64 KB ring, 2 CTAs/SM).  For the
+// paper's shape (G = 4, one group) a few alternatives are selectable for measurement
+// with ARKV_FAST_CFG=C,SPW (4,1 | 4,2 | 6,2 | 4,3 | 8,1).
+template <int G, int NG>
+static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+  if (G == 4 && NG == 1) {
+    const char* e = std::getenv("ARKV_FAST_CFG");
+    const int cfg = e ? (e[0] - '0') * 10 + (e[2] - '0') : 41;
+    switch (cfg) {
+      case 42: launch_cfg<G, NG, 4, 2>(a, n_units_call, s, ev0, ev1); return;
+      case 62: launch_cfg<G, NG, 6, 2>(a, n_units_call, s, ev0, ev1); return;
+      case 43: launch_cfg<G, NG, 4, 3>(a, n_units_call, s, ev0, ev1); return;
+      case 81: launch_cfg<G, NG, 8, 1>(a, n_units_call, s, ev0, ev1); return;
+      default: break;
+    }
+  }
+  launch_cfg<G, NG, 4, 1>(a, n_units_call, s, ev0, ev1);
 }
 
 template <int G>

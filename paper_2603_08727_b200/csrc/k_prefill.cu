@@ -12,6 +12,8 @@
 // A third tiny kernel reduces those columns into entropy / variance / kurtosis and
 // the OQ score in float64 (Eqs. 3-6; R2-R7), in a fixed order
 // (bitwise deterministic).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace arkv {
@@ -357,8 +359,19 @@ static int launch_passes(const Geom& g, const uint16_t* q_win, const uint16_t* k
   return 2;
 }
 
+bool prefill_tc_available(const Geom& g);  // k_prefill_tc.cu
+int launch_prefill_tc(const Geom& g, const uint16_t* q_win, const uint16_t* k, int P, float2* partials, int n_chunks1,
+                      float2* acc_pf, cudaStream_t s);
+
 int launch_prefill_begin(const Geom& g, const uint16_t* q_win, const uint16_t* k, int P, float* partials,
                          int n_chunks1, float2* acc_pf, double* colsum, cudaStream_t s) {
+  const char* env = std::getenv("ARKV_PREFILL_TC");
+  if (prefill_tc_available(g) && !(env && env[0] == '0')) {  // tcgen05 passes (G*W = 128, d = 128)
+    const int n = launch_prefill_tc(g, q_win, k, P, (float2*)partials, n_chunks1, acc_pf, s);
+    dim3 grid((P - g.W + 255) / 256, g.batch * g.L);
+    prefill_colsum_kernel<<<grid, 256, 0, s>>>(g, acc_pf, P, colsum);
+    return n + 1;
+  }
   const int R = g.G * g.W;
   const int mtiles = (R + 15) / 16;
   const bool two = (mtiles % 2 == 0) && mtiles >= 2;

@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
   __shared__ uint32_t hist[2][256];
   __shared__ uint64_t sh_prefix[2];
   __shared__ uint32_t sh_rem[2];
+  griddep_wait();
   const TailorJob jb = jobs.j[blockIdx.x];
   int8_t* st = st_scratch + (int64_t)blockIdx.x * st_stride;  // [old O rows | old Q rows]
   const int n_elig_o = jb.n_o_old - jb.n_win_old;
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(1024) tailor_scan_kernel(Geom g, TailorJobs jo
                                                            int32_t* __restrict__ src_scratch, int src_stride,
                                                            int32_t* err) {
   __shared__ int2 sh[33];
+  griddep_wait();
   const TailorJob jb = jobs.j[blockIdx.x];
   const int8_t* st = st_scratch + (int64_t)blockIdx.x * st_stride;
   const int q_off = st_stride - g.cap_q;
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g, TailorJobs job
                                                           const uint16_t* __restrict__ pv, int P,
                                                           const int32_t* __restrict__ src_scratch, int src_stride) {
   extern __shared__ __align__(16) uint8_t tile[];
+  griddep_wait();
   const TailorJob jb = jobs.j[blockIdx.y];
   const int n_o_new = jb.n_oe + jb.n_win_old;
   const int tiles_o = (n_o_new + kTile - 1) / kTile;
@@ -476,15 +479,17 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
                   int8_t* st_scratch, int32_t* src_scratch, int32_t* err, cudaStream_t s) {
   const int st_stride = max(g.max_pos, g.cap_o) + g.cap_q;
   const int src_stride = g.cap_o + g.cap_q;
-  tailor_select_kernel<<<n_jobs, 1024, 0, s>>>(g, jobs, meta, acc_pf, st_scratch, st_stride);
-  tailor_scan_kernel<<<n_jobs, 1024, 0, s>>>(g, jobs, desc, st_scratch, st_stride, src_scratch, src_stride, err);
+  launch_pdl(tailor_select_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, meta, acc_pf, st_scratch, st_stride);
+  launch_pdl(tailor_scan_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, desc, (const int8_t*)st_scratch, st_stride,
+             src_scratch, src_stride, err);
   size_t smem = (size_t)max(g.tile_o, ((g.tile_q + 15) & ~15) + 2 * kTile * g.d);
   dim3 grid(max_tiles, n_jobs);
   const int vpl = (g.d + 31) / 32;
 #define MV_CASE(V)                                                                                                \
   case V:                                                                                                         \
     cudaFuncSetAttribute(tailor_move_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
-    tailor_move_kernel<V><<<grid, 256, smem, s>>>(g, jobs, slots, meta, pk, pv, P, src_scratch, src_stride);      \
+    launch_pdl(tailor_move_kernel<V>, grid, dim3(256), smem, s, g, jobs, slots, meta, pk, pv, P,                   \
+               (const int32_t*)src_scratch, src_stride);                                                         \
     break;
   switch (vpl) {
     MV_CASE(1)

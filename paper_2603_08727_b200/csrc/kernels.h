@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "common.cuh"
 
 namespace arkv {
@@ -56,6 +58,7 @@ struct DecodeArgs {
   int q_group;        // fast kernel: Quantized tiles per bulk copy (0 = as many as fit a stage)
   int interleave;     // fast kernel: interleave Original and Quantized work items
   int fuse_combine;   // fast kernel: the last split CTA of a unit merges the partials
+  int producer_mode;  // fast kernel: 0 refill stages in item order, 1 whichever frees first
   void* out;
   int out_fp32;
   int32_t* err;
@@ -70,6 +73,24 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
 }  // namespace arkv
 
 namespace arkv {
+// Launch with programmatic stream serialization (PDL): the kernel may begin while the
+// previous kernel on the stream drains; it calls griddep_wait() before dependent reads.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // k_decode_fast.cu: true when the tensor-core decode kernel supports this cache.
 bool decode_fast_available(const Geom& g);
 }  // namespace arkv
