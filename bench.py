@@ -156,7 +156,10 @@ def run_arkv(args, wl):
     K, Wm = args.steps, args.warmup
     n_e2e = args.e2e_steps
     total_steps = Wm + K + n_e2e
-    cfg = A.make_config(L, Hq, Hkv, d, batch=B, window=wl["window"], budget_tokens=wl["budget"],
+    budget = wl["budget"]
+    if args.mode == "base":            # Base: no cache limit -> every token stays bf16
+        budget = P + total_steps + 2 * wl["window"] + 1
+    cfg = A.make_config(L, Hq, Hkv, d, batch=B, window=wl["window"], budget_tokens=budget,
                         quant_bits=wl["bits"], group_size=wl["group"], max_positions=P + total_steps + 1,
                         max_prompt=P, decode_kernel=args.kernel)
     cache = A.ArkvCache(cfg, dev)
@@ -166,7 +169,12 @@ def run_arkv(args, wl):
     qw, k, v = prefill_inputs_fast(sh, seed=seed, device=dev)
     torch.cuda.synchronize()
     t0 = time.time()
-    stats, oq, rho = cache.arkv_prefill_stats(qw, k, v)
+    rho_override = None
+    if args.mode == "origin":          # Base_origin: budgeted heavy hitters, all bf16
+        rho_override = [[1.0] * L for _ in range(B)]
+    elif args.mode == "quant":         # Base_quant: every kept eligible token quantized
+        rho_override = [[0.0] * L for _ in range(B)]
+    stats, oq, rho = cache.arkv_prefill_stats(qw, k, v, rho_override=rho_override)
     cache.arkv_check()
     prefill_s = time.time() - t0
     del qw, k, v
@@ -277,6 +285,7 @@ def run_arkv(args, wl):
     else:
         rho_all = rho.reshape(-1)
     peak, peak_src = peaks()
+    read_ceiling = read_ceiling_gbs(dev) if not args.no_ceiling else None
     value = ws * B * K / (ms / 1e3)
     step_bytes = (cache_bytes_per_step(cache, wl, n_o0, n_q0) + cache_bytes_per_step(cache, wl, n_o1, n_q1)) / 2
     kernel_ms = k_ms / max(k_cnt, 1)
@@ -290,7 +299,7 @@ def run_arkv(args, wl):
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    budget_tokens = B * L * Hkv * wl["budget"]
+    budget_tokens = B * L * Hkv * budget
     evicted = float(((pos1 - n_o1 - n_q1)).sum())
     line = {
         "metric": METRIC,
@@ -307,7 +316,7 @@ def run_arkv(args, wl):
         "data": "synthetic (synth/ natural recipe: sinks, 5% log-normal heavy hitters, recency bump, x8 outlier V channels)",
         "config": {"workload": f"{args.workload} (BASELINE.json configs[{wl['baseline_cfg']}])",
                    "layers": L, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d, "batch_per_gpu": B,
-                   "global_batch": B * ws, "prompt_len": P, "budget_tokens": wl["budget"], "window": wl["window"],
+                   "global_batch": B * ws, "prompt_len": P, "budget_tokens": budget, "window": wl["window"], "mode": args.mode,
                    "quant": f"int{wl['bits']} g{wl['group']} asym", "alpha": 0.75,
                    "launch": "one arkv_decode_step per step covering all layers (layer-batched)",
                    "decode_kernel": "fast" if cache_fast(cache) else "generic",
@@ -320,6 +329,7 @@ def run_arkv(args, wl):
         "step_hbm": {"alg_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms / K / 1e3) / 1e9,
                      "frac_of_peak": step_bytes / (ms / K / 1e3) / 1e9 / peak,
                      "frac_of_8tbs_nominal": step_bytes / (ms / K / 1e3) / 1e12 / 8.0},
+        "read_ceiling": {"gbs": read_ceiling, "how": "best of torch amax/sum over a 2 GiB bf16 tensor (reference only)"},
         "gpu_launches": int(launches),
         "tailors_in_timed_region": int(tailors_timed),
         "memory": {"arena_bytes": cache.arena_bytes, "dense_bf16_bytes": B * L * Hkv * (P + total_steps) * 4 * d,
@@ -336,6 +346,27 @@ def run_arkv(args, wl):
     if ws > 1:
         dist.destroy_process_group()
     return line, rank
+
+
+def read_ceiling_gbs(dev) -> float:
+    """Reference read-only HBM ceiling: best of two torch reductions over 2 GiB."""
+    import torch
+    x = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev).uniform_()
+    best = 0.0
+    for fn in (lambda: x.amax(), lambda: x.sum(dtype=torch.float32)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 10 * x.numel() * 2 / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    del x
+    torch.cuda.empty_cache()
+    return best
 
 
 def cache_fast(cache) -> bool:
@@ -431,6 +462,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=-1, help="-1: same as --steps")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ceiling", action="store_true")
+    ap.add_argument("--mode", default="arkv", choices=["arkv", "base", "origin", "quant"],
+                    help="arkv (stats-driven rho) or the paper's baselines: base, origin (rho=1), quant (rho=0)")
     ap.add_argument("--prompt-len", type=int, default=0, help="debug: override the workload's prompt length")
     ap.add_argument("--layers", type=int, default=0, help="debug: override the workload's layer count")
     args = ap.parse_args()

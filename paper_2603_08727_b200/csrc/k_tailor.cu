@@ -301,13 +301,15 @@ __device__ __forceinline__ float read_o(const Geom& g, const uint8_t* tile, int 
   return bf16_to_f(*(const uint16_t*)(tile + off));
 }
 
-template <int VPL>  // values per lane = ceil(d / 32)
-__global__ void __launch_bounds__(256) tailor_move_kernel(Geom g, TailorJobs jobs, uint8_t* slots, uint8_t* meta,
+template <int VPL, int DC>  // values per lane = ceil(d / 32); DC = compile-time head dim (0: runtime)
+__global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs jobs, uint8_t* slots, uint8_t* meta,
                                                           const uint16_t* __restrict__ pk,
                                                           const uint16_t* __restrict__ pv, int P,
                                                           const int32_t* __restrict__ src_scratch, int src_stride) {
   extern __shared__ __align__(16) uint8_t tile[];
   griddep_wait();
+  Geom g = g_in;
+  if (DC) g.d = DC;  // lets the tile-layout index maps fold their divisions into shifts
   const TailorJob jb = jobs.j[blockIdx.y];
   const int n_o_new = jb.n_oe + jb.n_win_old;
   const int tiles_o = (n_o_new + kTile - 1) / kTile;
@@ -335,6 +337,9 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g, TailorJobs job
   const int qmaxv = (1 << (g.bits - 1)) - 1;
   const int off = g.mode == ARKV_QUANT_SYM ? (1 << (g.bits - 1)) : 0;
 
+  int gidx[VPL];  // quantization group of each of this lane's dims
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) gidx[t] = (lane + 32 * t) / g.g;
   for (int j = warp; j < kTile; j += blockDim.x >> 5) {
     const int row = tid * kTile + j;
     if (row >= n_new) continue;
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g, TailorJobs job
 #pragma unroll
         for (int t = 0; t < VPL; ++t) {
           int x = lane + 32 * t;
-          if (x < g.d && x / g.g == grp) {
+          if (x < g.d && gidx[t] == grp) {
             float v = kvv[kv][t];
             mn = fminf(mn, v);
             mx = fmaxf(mx, v);
@@ -444,7 +449,7 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g, TailorJobs job
 #pragma unroll
         for (int t = 0; t < VPL; ++t) {
           int x = lane + 32 * t;
-          if (x < g.d && x / g.g == grp) {
+          if (x < g.d && gidx[t] == grp) {
             int c;
             if (flat) {
               c = 0;
@@ -485,12 +490,18 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
   size_t smem = (size_t)max(g.tile_o, ((g.tile_q + 15) & ~15) + 2 * kTile * g.d);
   dim3 grid(max_tiles, n_jobs);
   const int vpl = (g.d + 31) / 32;
-#define MV_CASE(V)                                                                                                \
-  case V:                                                                                                         \
-    cudaFuncSetAttribute(tailor_move_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
-    launch_pdl(tailor_move_kernel<V>, grid, dim3(256), smem, s, g, jobs, slots, meta, pk, pv, P,                   \
-               (const int32_t*)src_scratch, src_stride);                                                         \
+#define MV_LAUNCH(V, DCV)                                                                                         \
+  cudaFuncSetAttribute(tailor_move_kernel<V, DCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+  launch_pdl(tailor_move_kernel<V, DCV>, grid, dim3(256), smem, s, g, jobs, slots, meta, pk, pv, P,                 \
+             (const int32_t*)src_scratch, src_stride);
+#define MV_CASE(V)       \
+  case V:                \
+    MV_LAUNCH(V, 0)      \
     break;
+  if (g.d == 128) {
+    MV_LAUNCH(4, 128)
+    return 3;
+  }
   switch (vpl) {
     MV_CASE(1)
     MV_CASE(2)
@@ -500,6 +511,7 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
       return -1;
   }
 #undef MV_CASE
+#undef MV_LAUNCH
   return 3;
 }
 
