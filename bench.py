@@ -295,7 +295,7 @@ def run_arkv(args, wl):
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
-            if tj.get("workload") == args.workload and tj.get("kernel_impl") == ("fast" if cache_fast(cache) else "generic"):
+            if tj.get("workload") == args.workload and tj.get("kernel_impl") == cache_kernel(cache):
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -319,7 +319,7 @@ def run_arkv(args, wl):
                    "global_batch": B * ws, "prompt_len": P, "budget_tokens": budget, "window": wl["window"], "mode": args.mode,
                    "quant": f"int{wl['bits']} g{wl['group']} asym", "alpha": 0.75,
                    "launch": "one arkv_decode_step per step covering all layers (layer-batched)",
-                   "decode_kernel": "fast" if cache_fast(cache) else "generic",
+                   "decode_kernel": cache_kernel(cache),
                    "parallelism": f"dp{ws} (whole sequences per GPU, no collective in the loop)",
                    "l2": "no flush: cache arena %.2f GB >> 126 MB L2" % (cache.arena_bytes / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -369,9 +369,9 @@ def read_ceiling_gbs(dev) -> float:
     return best
 
 
-def cache_fast(cache) -> bool:
+def cache_kernel(cache) -> str:
     from paper_2603_08727_b200 import arkv as A
-    return A.lib().arkv_cache_info(cache.handle, 1) == 1
+    return {0: "generic", 1: "fast", 2: "persistent"}[A.lib().arkv_cache_info(cache.handle, 1)]
 
 
 def cpu_baseline(wl, rho_seq, samples=4):
@@ -458,7 +458,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="arkv", choices=["arkv", "reference"])
     ap.add_argument("--workload", default="llama3-8b-32k", choices=sorted(WORKLOADS))
-    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 generic, 2 fast")
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 generic, 2 fast split-K, 3 fast persistent")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="-1: same as --steps")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

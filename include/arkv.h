@@ -73,7 +73,8 @@ typedef struct arkv_config {
   int32_t layout;        /* ARKV_LAYOUT_* (AUTO: FRAG when d % 32 == 0 and bits == 4) */
   int32_t n_spare_slots; /* tailor staging slots (0 -> batch * n_kv_heads) */
   int32_t max_splits;    /* split-K fan-out cap of the decode kernel (0 -> 64) */
-  int32_t decode_kernel; /* 0 auto (tensor-core kernel for FRAG 4-bit d=128), 1 generic, 2 fast */
+  int32_t decode_kernel; /* 0 auto (tensor-core kernel for FRAG 4-bit d=128), 1 generic, 2 fast split-K,
+                           3 fast persistent (range-partitioned) */
   double alpha;          /* slack factor, 0.75 */
   double tau[3];         /* OQ temperatures 7.774, 5.407, 5.528 */
   double gamma;          /* HH variance weight 263.81 */
@@ -201,7 +202,8 @@ arkv_status arkv_profile_read(arkv_cache* cache, int32_t which, double* total_ms
                               double* alg_bytes);
 
 /* Introspection: what = 0 -> tile layout in use (ARKV_LAYOUT_PLAIN / _FRAG);
-   1 -> decode kernel in use (0 generic, 1 tensor-core fast kernel).  -1 on error. */
+   1 -> decode kernel in use (0 generic, 1 tensor-core split-K kernel, 2 tensor-core
+   persistent kernel).  -1 on error. */
 int32_t arkv_cache_info(const arkv_cache* cache, int32_t what);
 
 /* Number of kernel launches issued by this cache so far (bench accounting). */

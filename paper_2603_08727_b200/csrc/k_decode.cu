@@ -337,8 +337,12 @@ void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s
 int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, const uint16_t* k, const uint16_t* v,
                   void* out, int out_fp32, uint8_t* slots, uint8_t* meta, UnitDesc* desc, float* partials,
                   float* logits, float* mstat, int32_t* counters, int acc_rows, int n_splits, int max_splits,
-                  int fast, int32_t* err, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+                  int fast, int32_t* err, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, const PlanArgs& plan) {
   DecodeArgs a;
+  a.plan = fast ? plan.plan : nullptr;
+  a.plan_U = plan.U;
+  a.plan_P = plan.P;
+  a.pparts = plan.pparts;
   a.g = g;
   a.layer0 = layer0;
   a.n_layers = n_layers;

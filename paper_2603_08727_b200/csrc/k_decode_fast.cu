@@ -193,6 +193,295 @@ __device__ __forceinline__ void make_b(const float (&v)[4], int t, uint32_t& b01
   c01 = c23 = 0u;
 }
 
+// ---- consumer building blocks (split kernel and persistent kernel) --------------------
+// q fragments of one unit: bf16 for Original tiles; f16 (with the 1/16 odd-nibble factor)
+// for Quantized tiles; Σq per group for the zero-point term (this thread's two heads
+// 2t, 2t+1 — only lanes with tq < G/2 matter).
+template <int NG>
+struct QFrag {
+  uint32_t qb[8][2], qh[8][2];
+  float qsum[2][NG];
+};
+template <int G, int NG>
+__device__ __forceinline__ void load_qfrag(const uint16_t* qp, int lane, QFrag<NG>& f) {
+  const int gq = lane >> 2, tq = lane & 3;
+  const int hq = gq;  // B operand column n = head gq
+  const bool hv = hq < G;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int x0 = tq * 32 + 4 * c;  // Original tiles: dims t*(d/4)+4c+{0,1} / +{2,3}
+    f.qb[c][0] = hv ? *(const uint32_t*)(qp + hq * D + x0) : 0u;
+    f.qb[c][1] = hv ? *(const uint32_t*)(qp + hq * D + x0 + 2) : 0u;
+    // Quantized tiles: chunk c = 2jp + cc; nibble pairs (e, e+4) with e = 2cc (+1 for b1)
+    const int jp = c >> 1, cc = c & 1;
+    const int xb = 32 * jp + 8 * tq + 2 * cc;
+    float f0 = hv ? bf16_to_f(qp[hq * D + xb + 0]) : 0.f, f4 = hv ? bf16_to_f(qp[hq * D + xb + 4]) : 0.f;
+    float f1 = hv ? bf16_to_f(qp[hq * D + xb + 1]) : 0.f, f5 = hv ? bf16_to_f(qp[hq * D + xb + 5]) : 0.f;
+    f.qh[c][0] = pack_f16(f0, f4);
+    f.qh[c][1] = pack_f16(f1 * 0.0625f, f5 * 0.0625f);
+  }
+  // Σ_x q[h][x] per group: lane sums its 4 dims, segmented butterfly over the 32/NG lanes
+  // of each group, then the owner lanes pick their heads' sums
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+#pragma unroll
+    for (int gr = 0; gr < NG; ++gr) f.qsum[e][gr] = 0.f;
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float v = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v += bf16_to_f(qp[h * D + lane * 4 + i]);
+#pragma unroll
+    for (int off = 1; off < 32 / NG; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+#pragma unroll
+    for (int gr = 0; gr < NG; ++gr) {
+      const float sgr = __shfl_sync(0xffffffffu, v, gr * (32 / NG));
+      if (2 * tq == h) f.qsum[0][gr] = sgr;
+      if (2 * tq + 1 == h) f.qsum[1][gr] = sgr;
+    }
+  }
+}
+
+// Running flash state of one consumer warp: O^T accumulators (m-tile over dims,
+// (dim g|g+8) x (col 2t|2t+1)) and, per head 2t+e, the running max (log2 domain), Σp and
+// Σ p·z_v per group.
+template <int NG>
+struct Acc {
+  float o[8][4];
+  float m_run[2], l_run[2];
+  float z_run[2][NG];
+};
+template <int NG>
+__device__ __forceinline__ void acc_reset(Acc<NG>& s) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s.o[i][e] = 0.f;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    s.m_run[e] = -INFINITY;
+    s.l_run[e] = 0.f;
+#pragma unroll
+    for (int gr = 0; gr < NG; ++gr) s.z_run[e][gr] = 0.f;
+  }
+}
+
+// Folds one staged 32-token tile into the warp's flash state.  tb: the tile in shared
+// memory; n_valid: rows in use; lrow: HH logit row base of this tile (a.logits + (u G)
+// row_stride + (isq ? cap_o : 0) + 32 tile) or nullptr outside the HH window.
+template <int G, int NG>
+__device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_valid, float* lrow, int row_stride,
+                                             const QFrag<NG>& f, Acc<NG>& s, float c2, bool sym, int lane,
+                                             int src_lane) {
+  const int gq = lane >> 2, tq = lane & 3;
+  // ---- S = K q^T, logits in the log2 domain ----
+  float lg[2][4];      // [m-tile][(row g|g+8) x (col 2t|2t+1)]
+  float zv[2][2][NG];  // Quantized: z_v of rows (g, g+8) per m-tile, per group
+  if (!isq) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int qd = 0; qd < 4; ++qd) {
+        const uint4 r0 = lds128(tb + (((mt * 2 + 0) * 4 + qd) * 32 + lane) * 16);
+        const uint4 r1 = lds128(tb + (((mt * 2 + 1) * 4 + qd) * 32 + lane) * 16);
+        mma_bf16(acc, r0.x, r1.x, r0.y, r1.y, f.qb[2 * qd][0], f.qb[2 * qd][1]);
+        mma_bf16(acc, r0.z, r1.z, r0.w, r1.w, f.qb[2 * qd + 1][0], f.qb[2 * qd + 1][1]);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) lg[mt][e] = acc[e] * c2;
+    }
+  } else {
+    const float* sc = (const float*)(tb + 32 * D);  // [which][grp][32]
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      float acc[NG][4];
+#pragma unroll
+      for (int gr = 0; gr < NG; ++gr)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[gr][e] = 0.f;
+      const uint4 r0 = lds128(tb + ((mt * 2 + 0) * 32 + lane) * 16);
+      const uint4 r1 = lds128(tb + ((mt * 2 + 1) * 32 + lane) * 16);
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {
+        uint32_t x[4], y[4];
+        unpack8(word(r0, jp), x);
+        unpack8(word(r1, jp), y);
+        const int gr = (jp * 32) / (D / NG);
+        mma_f16(acc[gr], x[0], y[0], x[1], y[1], f.qh[2 * jp][0], f.qh[2 * jp][1]);
+        mma_f16(acc[gr], x[2], y[2], x[3], y[3], f.qh[2 * jp + 1][0], f.qh[2 * jp + 1][1]);
+      }
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int j = mt * 16 + gq + 8 * hh;
+        float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+        for (int gr = 0; gr < NG; ++gr) {
+          const float ks = sc[(0 * NG + gr) * 32 + j];
+          float kz = sc[(1 * NG + gr) * 32 + j];
+          const float vs = sc[(2 * NG + gr) * 32 + j];
+          float vz = sc[(3 * NG + gr) * 32 + j];
+          if (sym) {
+            kz = -8.f * ks;
+            vz = -8.f * vs;
+          }
+          l0 += ks * acc[gr][hh * 2 + 0] + kz * f.qsum[0][gr];
+          l1 += ks * acc[gr][hh * 2 + 1] + kz * f.qsum[1][gr];
+          zv[mt][hh][gr] = vz;
+        }
+        lg[mt][hh * 2 + 0] = l0 * c2;
+        lg[mt][hh * 2 + 1] = l1 * c2;
+      }
+    }
+  }
+  // mask rows beyond the segment (and padding heads)
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = mt * 16 + gq + 8 * (e >> 1);
+      const int h = 2 * tq + (e & 1);
+      if (j >= n_valid || h >= G) lg[mt][e] = -INFINITY;
+    }
+  if (lrow) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = mt * 16 + gq + 8 * (e >> 1);
+        const int h = 2 * tq + (e & 1);
+        if (j < n_valid && h < G) lrow[(int64_t)h * row_stride + j] = lg[mt][e];
+      }
+  }
+  // ---- online softmax (per head = per (tq, e)) ----
+  float tmax[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    float mx = fmaxf(fmaxf(lg[0][e], lg[0][e + 2]), fmaxf(lg[1][e], lg[1][e + 2]));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    tmax[e] = mx;
+  }
+  float corr[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const float mn = fmaxf(s.m_run[e], tmax[e]);
+    corr[e] = (mn == -INFINITY) ? 1.f : exp2f(s.m_run[e] - mn);
+    s.m_run[e] = mn;
+    s.l_run[e] *= corr[e];
+#pragma unroll
+    for (int gr = 0; gr < NG; ++gr) s.z_run[e][gr] *= corr[e];
+  }
+  // rescale O^T columns: col 2t+e belongs to head (2t+e) % G, whose max lives in lane src_lane
+  {
+    const float c0 = __shfl_sync(0xffffffffu, corr[0], src_lane);
+    const float c1 = __shfl_sync(0xffffffffu, G >= 2 ? corr[1] : corr[0], src_lane);
+#pragma unroll
+    for (int mv = 0; mv < 8; ++mv) {
+      s.o[mv][0] *= c0;
+      s.o[mv][1] *= c1;
+      s.o[mv][2] *= c0;
+      s.o[mv][3] *= c1;
+    }
+  }
+  float p[2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float mm = s.m_run[e & 1];
+      p[mt][e] = (lg[mt][e] == -INFINITY) ? 0.f : exp2f(lg[mt][e] - mm);
+      s.l_run[e & 1] += p[mt][e];
+    }
+
+  if (!isq) {
+    // ---- PV on Original tiles (bf16) ----
+    if (n_valid < kTile) {
+      // rows past the segment may hold stale bytes (NaN patterns): P' = 0 there, but
+      // 0 * NaN = NaN inside the MMA, so zero them in the staged copy
+      uint8_t* tw = const_cast<uint8_t*>(tb);
+      for (int idx = lane; idx < (kTile - n_valid) * D; idx += 32) {
+        const int j = n_valid + idx / D, x = idx % D;
+        // FRAG V offset (common.cuh o_v_off) for d = 128
+        const int mtv = x >> 4, r = x & 15, gg = r & 7, sel = r >> 3;
+        const int kc = j >> 4, jj = j & 15, hi = jj >> 3, tt = jj & 7, t = tt >> 1, uu = tt & 1;
+        const int k = (mtv * 2 + kc) * 4 + sel + 2 * hi;
+        *(uint16_t*)(tw + 64 * D + lane_word(k, 4 * gg + t) * 4 + uu * 2) = 0;
+      }
+      // order these generic-proxy writes before the stage's next TMA (async-proxy) fill
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+    }
+    uint32_t b01[2], b23[2], c01[2], c23[2];
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) make_b<G, true>(p[kc], tq, b01[kc], b23[kc], c01[kc], c23[kc]);
+    const uint8_t* vb = tb + 64 * D;
+#pragma unroll
+    for (int mv = 0; mv < 8; ++mv) {
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc) {
+        const uint4 r = lds128(vb + ((mv * 2 + kc) * 32 + lane) * 16);
+        mma_bf16(s.o[mv], r.x, r.y, r.z, r.w, b01[kc], b23[kc]);
+        if (G == 8) mma_bf16(s.o[mv], r.x, r.y, r.z, r.w, c01[kc], c23[kc]);
+      }
+    }
+  } else {
+    // ---- PV on Quantized tiles (f16 codes, P' = p·s_v / f) ----
+    const float* sc = (const float*)(tb + 32 * D);
+    uint32_t b01[NG][2], b23[NG][2], c01[NG][2], c23[NG][2];
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) {
+#pragma unroll
+      for (int gr = 0; gr < NG; ++gr) {
+        float vsc[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) vsc[hh] = sc[(2 * NG + gr) * 32 + kc * 16 + gq + 8 * hh];
+        float pv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pv[e] = p[kc][e] * vsc[e >> 1] * ((e >> 1) ? 0.0625f : 1.f);
+        make_b<G, false>(pv, tq, b01[gr][kc], b23[gr][kc], c01[gr][kc], c23[gr][kc]);
+        // zero-point term Σ p·z_v
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s.z_run[e & 1][gr] += p[kc][e] * zv[kc][e >> 1][gr];
+      }
+    }
+    const uint8_t* vb = tb + 16 * D;
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd) {
+      const uint4 r = lds128(vb + (qd * 32 + lane) * 16);
+#pragma unroll
+      for (int hm = 0; hm < 2; ++hm) {
+        const int mv = 2 * qd + hm;
+        const int gr = (mv * 16) / (D / NG);
+        uint32_t x[4], y[4];
+        unpack8(word(r, 2 * hm + 0), x);  // dim row g
+        unpack8(word(r, 2 * hm + 1), y);  // dim row g+8
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) {
+          mma_f16(s.o[mv], x[2 * kc], y[2 * kc], x[2 * kc + 1], y[2 * kc + 1], b01[gr][kc], b23[gr][kc]);
+          if (G == 8)
+            mma_f16(s.o[mv], x[2 * kc], y[2 * kc], x[2 * kc + 1], y[2 * kc + 1], c01[gr][kc], c23[gr][kc]);
+        }
+      }
+    }
+  }
+}
+
+// Reduces l and z over the 8 row lanes (every lane ends with its heads' sums).
+template <int NG>
+__device__ __forceinline__ void acc_reduce_rows(Acc<NG>& s) {
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      s.l_run[e] += __shfl_xor_sync(0xffffffffu, s.l_run[e], off);
+#pragma unroll
+      for (int gr = 0; gr < NG; ++gr) s.z_run[e][gr] += __shfl_xor_sync(0xffffffffu, s.z_run[e][gr], off);
+    }
+  }
+}
+
 template <int G, int NG, int C, int SPW>
 __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536) ? 2 : 1)
     decode_fast_kernel(DecodeArgs a) {
@@ -320,64 +609,16 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536)
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) sm.newtok[0][h] = acc * c2;
       }
+      __syncwarp();
       if (accm && lane < G)
         a.logits[((int64_t)u * G + lane) * row_stride + n_o] = sm.newtok[0][lane];
     }
   } else {
     // ===================== consumers =====================
-    // q fragments: bf16 for Original tiles; f16 (with the 1/16 odd-nibble factor) for
-    // Quantized tiles; Σq per group for the zero-point term.
-    uint32_t qb[8][2], qh[8][2];
-    float qsum[2][NG];  // this thread's two heads (2t, 2t+1) — only lanes with tq < G/2 matter
-    {
-      const int hq = gq;  // B operand column n = head gq
-      const bool hv = hq < G;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int x0 = tq * 32 + 4 * c;  // Original tiles: dims t*(d/4)+4c+{0,1} / +{2,3}
-        qb[c][0] = hv ? *(const uint32_t*)(qp + hq * D + x0) : 0u;
-        qb[c][1] = hv ? *(const uint32_t*)(qp + hq * D + x0 + 2) : 0u;
-        // Quantized tiles: chunk c = 2jp + cc; nibble pairs (e, e+4) with e = 2cc (+1 for b1)
-        const int jp = c >> 1, cc = c & 1;
-        const int xb = 32 * jp + 8 * tq + 2 * cc;
-        float f0 = hv ? bf16_to_f(qp[hq * D + xb + 0]) : 0.f, f4 = hv ? bf16_to_f(qp[hq * D + xb + 4]) : 0.f;
-        float f1 = hv ? bf16_to_f(qp[hq * D + xb + 1]) : 0.f, f5 = hv ? bf16_to_f(qp[hq * D + xb + 5]) : 0.f;
-        qh[c][0] = pack_f16(f0, f4);
-        qh[c][1] = pack_f16(f1 * 0.0625f, f5 * 0.0625f);
-      }
-      // Σ_x q[h][x] per group: lane sums its 4 dims, segmented butterfly over the
-      // 32/NG lanes of each group, then the owner lanes pick their heads' sums
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-#pragma unroll
-        for (int gr = 0; gr < NG; ++gr) qsum[e][gr] = 0.f;
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-        float v = 0.f;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v += bf16_to_f(qp[h * D + lane * 4 + i]);
-#pragma unroll
-        for (int off = 1; off < 32 / NG; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-#pragma unroll
-        for (int gr = 0; gr < NG; ++gr) {
-          const float sgr = __shfl_sync(0xffffffffu, v, gr * (32 / NG));
-          if (2 * tq == h) qsum[0][gr] = sgr;
-          if (2 * tq + 1 == h) qsum[1][gr] = sgr;
-        }
-      }
-    }
-    float o[8][4];  // O^T accumulators: m-tile over dims, (dim g|g+8) x (col 2t|2t+1)
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) o[i][e] = 0.f;
-    float m_run[2] = {-INFINITY, -INFINITY};  // heads 2t, 2t+1
-    float l_run[2] = {0.f, 0.f};
-    float z_run[2][NG];
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-#pragma unroll
-      for (int gr = 0; gr < NG; ++gr) z_run[e][gr] = 0.f;
+    QFrag<NG> qf;
+    load_qfrag<G, NG>(qp, lane, qf);
+    Acc<NG> acc;
+    acc_reset(acc);
     // lane holding the running max of the heads of this thread's O^T columns
     const int src_t = G >= 2 ? ((2 * tq) % G) / 2 : 0;
     const int src_lane = (lane & ~3) | src_t;
@@ -390,221 +631,26 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536)
       int first, ntiles;
       item_of(i, isq, first, ntiles);
       for (int jt = 0; jt < ntiles; ++jt) {
-      const uint8_t* tb = sm.ring[st] + (isq ? (ntiles - 1 - jt) * g.tile_q : 0);
-      const int tile = first + jt;
-      const int n_valid = isq ? min(kTile, n_q - tile * kTile) : min(kTile, n_o - tile * kTile);
-
-      // ---- S = K q^T, logits in the log2 domain ----
-      float lg[2][4];  // [m-tile][(row g|g+8) x (col 2t|2t+1)]
-      float zv[2][2][NG];  // Quantized: z_v of rows (g, g+8) per m-tile, per group
-      if (!isq) {
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int qd = 0; qd < 4; ++qd) {
-            const uint4 r0 = lds128(tb + (((mt * 2 + 0) * 4 + qd) * 32 + lane) * 16);
-            const uint4 r1 = lds128(tb + (((mt * 2 + 1) * 4 + qd) * 32 + lane) * 16);
-            mma_bf16(acc, r0.x, r1.x, r0.y, r1.y, qb[2 * qd][0], qb[2 * qd][1]);
-            mma_bf16(acc, r0.z, r1.z, r0.w, r1.w, qb[2 * qd + 1][0], qb[2 * qd + 1][1]);
-          }
-#pragma unroll
-          for (int e = 0; e < 4; ++e) lg[mt][e] = acc[e] * c2;
-        }
-      } else {
-        const float* sc = (const float*)(tb + 32 * D);  // [which][grp][32]
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          float acc[NG][4];
-#pragma unroll
-          for (int gr = 0; gr < NG; ++gr)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[gr][e] = 0.f;
-          const uint4 r0 = lds128(tb + ((mt * 2 + 0) * 32 + lane) * 16);
-          const uint4 r1 = lds128(tb + ((mt * 2 + 1) * 32 + lane) * 16);
-#pragma unroll
-          for (int jp = 0; jp < 4; ++jp) {
-            uint32_t x[4], y[4];
-            unpack8(word(r0, jp), x);
-            unpack8(word(r1, jp), y);
-            const int gr = (jp * 32) / (D / NG);
-            mma_f16(acc[gr], x[0], y[0], x[1], y[1], qh[2 * jp][0], qh[2 * jp][1]);
-            mma_f16(acc[gr], x[2], y[2], x[3], y[3], qh[2 * jp + 1][0], qh[2 * jp + 1][1]);
-          }
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int j = mt * 16 + gq + 8 * hh;
-            float l0 = 0.f, l1 = 0.f;
-#pragma unroll
-            for (int gr = 0; gr < NG; ++gr) {
-              const float ks = sc[(0 * NG + gr) * 32 + j];
-              float kz = sc[(1 * NG + gr) * 32 + j];
-              const float vs = sc[(2 * NG + gr) * 32 + j];
-              float vz = sc[(3 * NG + gr) * 32 + j];
-              if (sym) {
-                kz = -8.f * ks;
-                vz = -8.f * vs;
-              }
-              l0 += ks * acc[gr][hh * 2 + 0] + kz * qsum[0][gr];
-              l1 += ks * acc[gr][hh * 2 + 1] + kz * qsum[1][gr];
-              zv[mt][hh][gr] = vz;
-            }
-            lg[mt][hh * 2 + 0] = l0 * c2;
-            lg[mt][hh * 2 + 1] = l1 * c2;
-          }
-        }
+        const uint8_t* tb = sm.ring[st] + (isq ? (ntiles - 1 - jt) * g.tile_q : 0);
+        const int tile = first + jt;
+        const int n_valid = isq ? min(kTile, n_q - tile * kTile) : min(kTile, n_o - tile * kTile);
+        float* lrow = accm ? a.logits + (int64_t)u * G * row_stride + (isq ? g.cap_o : 0) + tile * kTile : nullptr;
+        consume_tile<G, NG>(tb, isq, n_valid, lrow, row_stride, qf, acc, c2, sym, lane, src_lane);
       }
-      // mask rows beyond the segment (and padding heads)
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j = mt * 16 + gq + 8 * (e >> 1);
-          const int h = 2 * tq + (e & 1);
-          if (j >= n_valid || h >= G) lg[mt][e] = -INFINITY;
-        }
-      if (accm) {
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int j = mt * 16 + gq + 8 * (e >> 1);
-            const int h = 2 * tq + (e & 1);
-            if (j < n_valid && h < G)
-              a.logits[((int64_t)u * G + h) * row_stride + (isq ? g.cap_o : 0) + tile * kTile + j] = lg[mt][e];
-          }
-      }
-      // ---- online softmax (per head = per (tq, e)) ----
-      float tmax[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        float mx = fmaxf(fmaxf(lg[0][e], lg[0][e + 2]), fmaxf(lg[1][e], lg[1][e + 2]));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-        tmax[e] = mx;
-      }
-      float corr[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const float mn = fmaxf(m_run[e], tmax[e]);
-        corr[e] = (mn == -INFINITY) ? 1.f : exp2f(m_run[e] - mn);
-        m_run[e] = mn;
-        l_run[e] *= corr[e];
-#pragma unroll
-        for (int gr = 0; gr < NG; ++gr) z_run[e][gr] *= corr[e];
-      }
-      // rescale O^T columns: col 2t+e belongs to head (2t+e) % G, whose max lives in lane src_lane
-      {
-        const float c0 = __shfl_sync(0xffffffffu, corr[0], src_lane);
-        const float c1 = __shfl_sync(0xffffffffu, G >= 2 ? corr[1] : corr[0], src_lane);
-#pragma unroll
-        for (int mv = 0; mv < 8; ++mv) {
-          o[mv][0] *= c0;
-          o[mv][1] *= c1;
-          o[mv][2] *= c0;
-          o[mv][3] *= c1;
-        }
-      }
-      float p[2][4];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float mm = m_run[e & 1];
-          p[mt][e] = (lg[mt][e] == -INFINITY) ? 0.f : exp2f(lg[mt][e] - mm);
-          l_run[e & 1] += p[mt][e];
-        }
-
-      if (!isq) {
-        // ---- PV on Original tiles (bf16) ----
-        if (n_valid < kTile) {
-          // rows past the segment may hold never-written bytes (NaN patterns): P' = 0
-          // there, but 0 * NaN = NaN inside the MMA, so zero them in the staged copy
-          uint8_t* tw = const_cast<uint8_t*>(tb);
-          for (int idx = lane; idx < (kTile - n_valid) * D; idx += 32)
-            *(uint16_t*)(tw + o_v_off(g, n_valid + idx / D, idx % D)) = 0;
-          // order these generic-proxy writes before the stage's next TMA (async-proxy) fill
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          __syncwarp();
-        }
-        uint32_t b01[2], b23[2], c01[2], c23[2];
-#pragma unroll
-        for (int kc = 0; kc < 2; ++kc) make_b<G, true>(p[kc], tq, b01[kc], b23[kc], c01[kc], c23[kc]);
-        const uint8_t* vb = tb + 64 * D;
-#pragma unroll
-        for (int mv = 0; mv < 8; ++mv) {
-#pragma unroll
-          for (int kc = 0; kc < 2; ++kc) {
-            const uint4 r = lds128(vb + ((mv * 2 + kc) * 32 + lane) * 16);
-            mma_bf16(o[mv], r.x, r.y, r.z, r.w, b01[kc], b23[kc]);
-            if (G == 8) mma_bf16(o[mv], r.x, r.y, r.z, r.w, c01[kc], c23[kc]);
-          }
-        }
-      } else {
-        // ---- PV on Quantized tiles (f16 codes, P' = p·s_v / f) ----
-        const float* sc = (const float*)(tb + 32 * D);
-        uint32_t b01[NG][2], b23[NG][2], c01[NG][2], c23[NG][2];
-#pragma unroll
-        for (int kc = 0; kc < 2; ++kc) {
-#pragma unroll
-          for (int gr = 0; gr < NG; ++gr) {
-            float vsc[2];
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) vsc[hh] = sc[(2 * NG + gr) * 32 + kc * 16 + gq + 8 * hh];
-            float pv[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) pv[e] = p[kc][e] * vsc[e >> 1] * ((e >> 1) ? 0.0625f : 1.f);
-            make_b<G, false>(pv, tq, b01[gr][kc], b23[gr][kc], c01[gr][kc], c23[gr][kc]);
-            // zero-point term Σ p·z_v
-#pragma unroll
-            for (int e = 0; e < 4; ++e) z_run[e & 1][gr] += p[kc][e] * zv[kc][e >> 1][gr];
-          }
-        }
-        const uint8_t* vb = tb + 16 * D;
-#pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-          const uint4 r = lds128(vb + (qd * 32 + lane) * 16);
-#pragma unroll
-          for (int hm = 0; hm < 2; ++hm) {
-            const int mv = 2 * qd + hm;
-            const int gr = (mv * 16) / (D / NG);
-            uint32_t x[4], y[4];
-            unpack8(word(r, 2 * hm + 0), x);  // dim row g
-            unpack8(word(r, 2 * hm + 1), y);  // dim row g+8
-#pragma unroll
-            for (int kc = 0; kc < 2; ++kc) {
-              mma_f16(o[mv], x[2 * kc], y[2 * kc], x[2 * kc + 1], y[2 * kc + 1], b01[gr][kc], b23[gr][kc]);
-              if (G == 8)
-                mma_f16(o[mv], x[2 * kc], y[2 * kc], x[2 * kc + 1], y[2 * kc + 1], c01[gr][kc], c23[gr][kc]);
-            }
-          }
-        }
-      }
-      }  // tiles of the item
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[st]);
     }
-
     // ---- per-warp finalisation: reduce l and z over the 8 row lanes ----
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {
-        l_run[e] += __shfl_xor_sync(0xffffffffu, l_run[e], off);
-#pragma unroll
-        for (int gr = 0; gr < NG; ++gr) z_run[e][gr] += __shfl_xor_sync(0xffffffffu, z_run[e][gr], off);
-      }
-    }
+    acc_reduce_rows(acc);
     if (gq == 0) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int h = 2 * tq + e;
         if (h < G) {
-          sm.wm[warp][h] = m_run[e];
-          sm.wl[warp][h] = l_run[e];
+          sm.wm[warp][h] = acc.m_run[e];
+          sm.wl[warp][h] = acc.l_run[e];
 #pragma unroll
-          for (int gr = 0; gr < NG; ++gr) sm.wz[warp][h][gr] = z_run[e][gr];
+          for (int gr = 0; gr < NG; ++gr) sm.wz[warp][h][gr] = acc.z_run[e][gr];
         }
       }
     }
@@ -614,10 +660,10 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536)
 #pragma unroll
     for (int mv = 0; mv < 8; ++mv) {
       const int x0 = mv * 16 + gq;
-      ob[(2 * tq + 0) * D + x0] = o[mv][0];
-      ob[(2 * tq + 1) * D + x0] = o[mv][1];
-      ob[(2 * tq + 0) * D + x0 + 8] = o[mv][2];
-      ob[(2 * tq + 1) * D + x0 + 8] = o[mv][3];
+      ob[(2 * tq + 0) * D + x0] = acc.o[mv][0];
+      ob[(2 * tq + 1) * D + x0] = acc.o[mv][1];
+      ob[(2 * tq + 0) * D + x0 + 8] = acc.o[mv][2];
+      ob[(2 * tq + 1) * D + x0 + 8] = acc.o[mv][3];
     }
   }
   __syncthreads();
@@ -714,6 +760,324 @@ static int launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaE
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Persistent, range-partitioned variant (decode_kernel = 3).
+// The step's items form two global streams — every unit's Original tiles, then every
+// unit's Quantized tiles in groups of q_per — and the host plan (PlanView) gives every CTA
+// an equal contiguous range of each, so all CTAs stream the same bytes of each kind with
+// one pipeline fill and drain.  The kernel is read-only on the cache: each consumer warp
+// flushes a partial (m, l, o) per (unit, phase) it touched, and decode_persist_combine
+// merges a unit's partials, appends the step's token and folds it in.
+// ---------------------------------------------------------------------------------------
+struct PUnit {
+  int u;  // global unit index
+  int slot, n_o, n_q, tiles_q;
+  bool accm;
+  const uint16_t* qp;
+};
+__device__ __forceinline__ void punit_load(const DecodeArgs& a, int ul, PUnit& p) {
+  const Geom& g = a.g;
+  const int b = ul / (a.n_layers * g.Hkv);
+  const int rem = ul % (a.n_layers * g.Hkv);
+  const int li = rem / g.Hkv, kvh = rem % g.Hkv;
+  p.u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
+  const UnitDesc dsc = a.desc[p.u];
+  p.slot = dsc.slot;
+  p.n_o = dsc.n_o;
+  p.n_q = dsc.n_q;
+  p.tiles_q = (p.n_q + kTile - 1) / kTile;
+  p.accm = (dsc.t_next >= dsc.trig - g.W) && (dsc.t_next < dsc.trig);
+  p.qp = a.q + ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * g.G) * D;
+}
+
+template <int G, int NG>
+__global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2) decode_persist_kernel(DecodeArgs a) {
+  constexpr int C = kPersistConsumers;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem<C, 1>& sm = *reinterpret_cast<Smem<C, 1>*>(smem_raw);
+  const Geom& g = a.g;
+  griddep_wait();  // PDL: the previous kernel (tailor / combine) has completed
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const PlanView pv(a.plan, a.plan_U, a.plan_P);
+  const int c = blockIdx.x;
+  const int lo0 = pv.cta_lo(0)[c], n0 = pv.cta_lo(0)[c + 1] - lo0;
+  const int lo1 = pv.cta_lo(1)[c], n1 = pv.cta_lo(1)[c + 1] - lo1;
+  const int n_work = n0 + n1;
+  const int q_per = kStageBytes / g.tile_q;
+  const int row_stride = g.cap_o + g.cap_q;
+  const float c2 = g.sm_scale * kLog2e;
+  const bool sym = g.mode == ARKV_QUANT_SYM;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (n_work <= 0) {
+    if (threadIdx.x == 0) griddep_launch_dependents();
+    return;
+  }
+  // item j of this CTA: phase f, stream index i; unit ul found by walking forward from hint
+  auto locate = [&](int j, int& f, int& i, int& ul, int hint_f, int hint_ul) {
+    f = j < n0 ? 0 : 1;
+    i = f == 0 ? lo0 + j : lo1 + (j - n0);
+    ul = (hint_f == f && hint_ul >= 0) ? hint_ul : pv.cta_u0(f)[c];
+    while (i >= pv.item_first(f)[ul + 1]) ++ul;
+  };
+
+  if (warp == C) {
+    // ===================== producer: the CTA's two ranges, in order =====================
+    if (lane == 0) {
+      int f = -1, ul = -1;
+      PUnit p;
+      p.u = -1;
+      for (int j = 0; j < n_work; ++j) {
+        int nf, i, nul;
+        locate(j, nf, i, nul, f, ul);
+        if (nul != ul || nf != f) {
+          punit_load(a, nul, p);
+          ul = nul;
+          f = nf;
+        }
+        const int st = j % C;
+        if (j >= C) mbar_wait(&sm.empty[st], ((j / C) - 1) & 1);
+        const int k = i - pv.item_first(f)[ul];
+        uint8_t* slot = a.slots + (int64_t)p.slot * g.slot_bytes;
+        const uint8_t* src;
+        uint32_t bytes;
+        if (f == 0) {
+          src = o_tile_ptr(slot, g, k);
+          bytes = (uint32_t)g.tile_o;
+        } else {
+          const int first = k * q_per, nt = min(q_per, p.tiles_q - first);
+          src = q_tile_ptr(slot, g, first + nt - 1);
+          bytes = (uint32_t)(nt * g.tile_q);
+        }
+        mbar_expect_tx(&sm.full[st], bytes);
+        bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
+      }
+      griddep_launch_dependents();  // PDL: the combine may start launching (it waits for us)
+    }
+    __syncwarp();
+    return;  // no CTA-wide barrier follows
+  }
+
+  // ===================== consumers =====================
+  const int src_t = G >= 2 ? ((2 * tq) % G) / 2 : 0;
+  const int src_lane = (lane & ~3) | src_t;
+  QFrag<NG> qf;
+  Acc<NG> acc;
+  PUnit p;
+  int cur = -1, curf = -1;
+  // partial of (unit cur, phase curf, this CTA, this warp): m, l and o (z term folded in)
+  auto flush = [&]() {
+    acc_reduce_rows(acc);
+    int slot_idx = pv.part_base()[cur] + (c - pv.cta_first(curf)[cur]) * C + warp;
+    if (curf == 1) slot_idx += (pv.cta_last(0)[cur] - pv.cta_first(0)[cur] + 1) * C;
+    float* part = a.pparts + (int64_t)slot_idx * G * (D + 2);
+#pragma unroll
+    for (int mv = 0; mv < 8; ++mv) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        // column 2t+(e&1) of dim row mv*16+gq+8(e>>1); for G < 8 columns h and h+G hold
+        // the hi and lo halves of head h's P'
+        float v = acc.o[mv][e];
+        if (G == 4) v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (G == 2) v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (G == 1) v += acc.o[mv][e ^ 1];
+        const int h = G == 1 ? 0 : 2 * tq + (e & 1);
+        const bool writer = G == 8 ? true : (G == 1 ? (tq == 0 && (e & 1) == 0) : (2 * tq < G));
+        if (writer && h < G) {
+          const int x = mv * 16 + gq + 8 * (e >> 1);
+          const int gr = x / (D / NG);
+          part[h * (D + 2) + 2 + x] = v + acc.z_run[e & 1][gr];
+        }
+      }
+    }
+    if (gq == 0) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int h = 2 * tq + e;
+        if (h < G) {
+          part[h * (D + 2) + 0] = acc.m_run[e];
+          part[h * (D + 2) + 1] = acc.l_run[e];
+        }
+      }
+    }
+  };
+  for (int j = warp; j < n_work; j += C) {
+    int f, i, ul;
+    locate(j, f, i, ul, curf, cur);
+    if (ul != cur || f != curf) {
+      if (cur >= 0) flush();
+      if (ul != cur) {
+        punit_load(a, ul, p);
+        load_qfrag<G, NG>(p.qp, lane, qf);
+      }
+      cur = ul;
+      curf = f;
+      acc_reset(acc);
+    }
+    const int st = j % C;
+    mbar_wait(&sm.full[st], (j / C) & 1);
+    __syncwarp();  // mma/movmatrix are .aligned
+    const int k = i - pv.item_first(f)[ul];
+    if (f == 0) {
+      float* lr = p.accm ? a.logits + (int64_t)p.u * G * row_stride + k * kTile : nullptr;
+      consume_tile<G, NG>(sm.ring[st], false, min(kTile, p.n_o - k * kTile), lr, row_stride, qf, acc, c2, sym,
+                          lane, src_lane);
+    } else {
+      const int first = k * q_per, nt = min(q_per, p.tiles_q - first);
+      for (int jt = 0; jt < nt; ++jt) {
+        const int tile = first + jt;
+        float* lr = p.accm ? a.logits + (int64_t)p.u * G * row_stride + g.cap_o + tile * kTile : nullptr;
+        consume_tile<G, NG>(sm.ring[st] + (nt - 1 - jt) * g.tile_q, true, min(kTile, p.n_q - tile * kTile), lr,
+                            row_stride, qf, acc, c2, sym, lane, src_lane);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[st]);
+  }
+  if (cur >= 0) flush();
+}
+
+// One CTA (D threads) per unit: append the step's token (D1), its logits (and HH logit
+// row), merge the unit's warp partials with it, write the output and the merged row
+// statistics, advance the descriptor.
+template <int G>
+__global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
+  griddep_wait();
+  griddep_launch_dependents();
+  constexpr int C = kPersistConsumers;
+  const Geom& g = a.g;
+  const PlanView pv(a.plan, a.plan_U, a.plan_P);
+  const int ul = blockIdx.x;
+  const int b = ul / (a.n_layers * g.Hkv);
+  const int rem = ul % (a.n_layers * g.Hkv);
+  const int li = rem / g.Hkv, kvh = rem % g.Hkv;
+  const int u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
+  const UnitDesc dsc = a.desc[u];
+  const int n_o = dsc.n_o, x = threadIdx.x, warp = x >> 5, lane = x & 31;
+  const int64_t qkv = (int64_t)(b * a.n_layers + li);
+  const uint16_t* qp = a.q + (qkv * g.Hq + kvh * G) * D;
+  const uint16_t* kn = a.k + (qkv * g.Hkv + kvh) * D;
+  const uint16_t* vn = a.v + (qkv * g.Hkv + kvh) * D;
+  const bool accm = (dsc.t_next >= dsc.trig - g.W) && (dsc.t_next < dsc.trig);
+  const int row_stride = g.cap_o + g.cap_q;
+  __shared__ float s_new[G], sM[G], sIL[G];
+  __shared__ float s_w[kMaxUnitParts][G];  // merge weight 2^(m - M) of each slot (0: unused)
+  // ---- append the token to the Original stack (row n_o) ----
+  const int tiles_o = (n_o + 1 + kTile - 1) / kTile, tiles_q = (dsc.n_q + kTile - 1) / kTile;
+  const bool fits = (n_o + 1 <= g.cap_o) && ((int64_t)tiles_o * g.tile_o + (int64_t)tiles_q * g.tile_q <= g.slot_bytes);
+  uint8_t* slot = a.slots + (int64_t)dsc.slot * g.slot_bytes;
+  const uint16_t kx = kn[x], vx = vn[x];
+  if (fits) {
+    uint8_t* tb = o_tile_ptr(slot, g, n_o / kTile);
+    *(uint16_t*)(tb + o_k_off(g, n_o % kTile, x)) = kx;
+    *(uint16_t*)(tb + o_v_off(g, n_o % kTile, x)) = vx;
+    if (x == 0) {
+      const SlotMeta meta = slot_meta(a.meta, g, dsc.slot);
+      meta.pos_o[n_o] = dsc.t_next;
+      meta.acc_o[n_o] = make_float2(0.f, 0.f);
+    }
+  } else if (x == 0) {
+    atomicOr(a.err, kErrCapacity);
+  }
+  // ---- its logits (log2 domain): warp w reduces heads w, w + 4 ----
+  const float c2 = g.sm_scale * kLog2e;
+  for (int h = warp; h < G; h += D / 32) {
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc = fmaf(bf16_to_f(qp[h * D + lane * 4 + i]), bf16_to_f(kn[lane * 4 + i]), acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      s_new[h] = acc * c2;
+      if (accm) a.logits[((int64_t)u * G + h) * row_stride + n_o] = acc * c2;
+    }
+  }
+  // ---- the unit's partial slots: C per covering CTA and phase, contiguous.  A slot whose
+  // warp processed none of the unit's items still holds l = 0 (slots start zeroed and
+  // every combine clears the l of the slots it merged), so validity is l > 0 ----
+  const int p0 = pv.part_base()[ul], ncand = min(pv.part_base()[ul + 1] - p0, kMaxUnitParts);
+  const float* pp = a.pparts + (int64_t)p0 * G * (D + 2);
+  __syncthreads();  // s_new
+  // merged max and sum per head: warp w reduces heads w, w + 4
+  for (int h = warp; h < G; h += D / 32) {
+    float M = s_new[h];
+    for (int k = lane; k < ncand; k += 32) {
+      const float* ph = pp + ((int64_t)k * G + h) * (D + 2);
+      if (__ldcg(ph + 1) > 0.f) M = fmaxf(M, __ldcg(ph));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float L = lane == 0 ? exp2f(s_new[h] - M) : 0.f;
+    for (int k = lane; k < ncand; k += 32) {
+      const float* ph = pp + ((int64_t)k * G + h) * (D + 2);
+      const float l = __ldcg(ph + 1);
+      const float w = l > 0.f ? exp2f(__ldcg(ph) - M) : 0.f;
+      s_w[k][h] = w;
+      L += l * w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (lane == 0) {
+      sM[h] = M;
+      sIL[h] = 1.0f / L;
+      a.mstat[((int64_t)u * G + h) * 2 + 0] = M;
+      a.mstat[((int64_t)u * G + h) * 2 + 1] = 1.0f / L;
+    }
+  }
+  __syncthreads();
+  const int64_t obase = (qkv * g.Hq + kvh * G) * D;
+  const float vnew = bf16_to_f(vx);
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float O = exp2f(s_new[h] - sM[h]) * vnew;
+    for (int k = 0; k < ncand; ++k) {
+      const float w = s_w[k][h];
+      if (w != 0.f) O += __ldcg(pp + ((int64_t)k * G + h) * (D + 2) + 2 + x) * w;
+    }
+    O *= sIL[h];
+    if (a.out_fp32)
+      ((float*)a.out)[obase + h * D + x] = O;
+    else
+      ((uint16_t*)a.out)[obase + h * D + x] = f_to_bf16_rne(O);
+  }
+  // clear the merged slots' l for the next step's plan
+  float* pw = a.pparts + (int64_t)p0 * G * (D + 2);
+  for (int k = x; k < ncand * G; k += D) pw[(int64_t)k * (D + 2) + 1] = 0.f;
+  if (x == 0) {
+    UnitDesc nd = dsc;
+    nd.n_o = n_o + 1;
+    nd.t_next = dsc.t_next + 1;
+    a.desc[u] = nd;
+  }
+}
+
+template <int G, int NG>
+static void launch_persist(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+  auto kern = decode_persist_kernel<G, NG>;
+  const int smem = (int)sizeof(Smem<kPersistConsumers, 1>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (ev0) cudaEventRecord(ev0, s);
+  launch_pdl(kern, dim3(a.plan_P), dim3((kPersistConsumers + 1) * 32), (size_t)smem, s, a);
+  if (ev1) cudaEventRecord(ev1, s);
+  launch_pdl(decode_persist_combine<G>, dim3(n_units_call), dim3(D), 0, s, a);
+}
+template <int G>
+static int launch_persist_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+  switch (a.g.ng) {
+    case 1: launch_persist<G, 1>(a, n_units_call, s, ev0, ev1); return 2;
+    case 2: launch_persist<G, 2>(a, n_units_call, s, ev0, ev1); return 2;
+    case 4: launch_persist<G, 4>(a, n_units_call, s, ev0, ev1); return 2;
+    default: return -1;
+  }
+}
+
 }  // namespace fast
 
 bool decode_fast_available(const Geom& g) {
@@ -725,6 +1089,15 @@ void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s
 
 int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
   if (!decode_fast_available(a.g)) return -1;
+  if (a.plan) {  // persistent range-partitioned kernel + its combine
+    switch (a.g.G) {
+      case 1: return fast::launch_persist_g<1>(a, n_units_call, s, ev0, ev1);
+      case 2: return fast::launch_persist_g<2>(a, n_units_call, s, ev0, ev1);
+      case 4: return fast::launch_persist_g<4>(a, n_units_call, s, ev0, ev1);
+      case 8: return fast::launch_persist_g<8>(a, n_units_call, s, ev0, ev1);
+      default: return -1;
+    }
+  }
   int r = -1;
   switch (a.g.G) {
     case 1: r = fast::launch_g<1>(a, n_units_call, s, ev0, ev1); break;

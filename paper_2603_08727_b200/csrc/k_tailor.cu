@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
     for (int i = threadIdx.x; i < 512; i += blockDim.x) (&hist[0][0])[i] = 0;
     const uint64_t p0 = sh_prefix[0], p1 = sh_prefix[1], m0 = sh_mask[0], m1 = sh_mask[1];
     const bool d0 = sh_done[0], d1 = sh_done[1];
+    // read before the digit search below rewrites it (one writer per selection and pass)
+    const uint32_t rem_in[2] = {sh_rem[0], sh_rem[1]};
     __syncthreads();
     const int sh = pass * 8;
     for (int i = threadIdx.x; i < n_e; i += blockDim.x) {
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
     __syncthreads();
     if (sel < 2 && !(sel ? d1 : d0)) {
       for (int w = 0; w < lw; ++w) incl += wsum[sel][w];
-      const uint32_t rem = sh_rem[sel], excl = incl - h;
+      const uint32_t rem = rem_in[sel], excl = incl - h;
       if (h > 0 && excl < rem && rem <= incl) {
         const int dgt = 255 - bi;
         sh_prefix[sel] |= ((uint64_t)dgt) << sh;

@@ -141,6 +141,47 @@ def test_generic_kernel_on_frag_layout():
     run_parity(MID, budget=512, steps=40, seed=6, rho=[[0.7, 0.3]], layout=2, decode_kernel=1, check_every=40)
 
 
+@pytest.mark.parametrize("g,mode", [(128, "asym"), (32, "asym"), (64, "sym")])
+def test_persistent_kernel_mid(g, mode):
+    """The persistent range-partitioned decode kernel (decode_kernel = 3) + its combine."""
+    r = run_parity(MID, budget=512, steps=80, seed=5, rho=[[1.0, 0.4]], layout=2, bits=4, g=g, mode=mode,
+                   decode_kernel=3, check_every=20)
+    assert r["tailors"] >= 2 * 2 * 2
+
+
+@pytest.mark.parametrize("G", [1, 2, 8])
+@pytest.mark.parametrize("kernel", [2, 3])
+def test_fast_kernels_gqa_groups(G, kernel):
+    """Tensor-core decode kernels (split-K and persistent) for GQA groups 1, 2, 8."""
+    sh = Shape(batch=2, n_layers=1, n_q_heads=2 * G, n_kv_heads=2, head_dim=128, prompt_len=1024, window=32)
+    r = run_parity(sh, budget=256, steps=48, seed=40 if G == 8 else 31 + G, rho=[[0.6], [0.3]], layout=2, bits=4, g=128,
+                   decode_kernel=kernel, check_every=16)
+    assert r["tailors"] >= 2
+
+
+def test_persistent_matches_split_states():
+    """Both fast kernels drive the same schedule: identical token states and codes, outputs
+    within the parity tolerance of each other (only the merge order differs)."""
+    from paper_2603_08727_b200 import arkv as A
+    sh = Shape(batch=2, n_layers=3, n_q_heads=16, n_kv_heads=4, head_dim=128, prompt_len=1500, window=32)
+    res = []
+    for kern in (2, 3):
+        cfg = A.make_config(3, 16, 4, 128, batch=2, budget_tokens=384, max_positions=1600, max_prompt=1500,
+                            decode_kernel=kern)
+        gpu = A.ArkvCache(cfg)
+        qw, k, v = prefill_inputs(sh, seed=41, recipe="margin")
+        gpu.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda())
+        outs = [gpu.arkv_decode_step(*[t.cuda() for t in decode_inputs(sh, s, seed=41, recipe="margin")], out_fp32=True).cpu()
+                for s in range(60)]
+        gpu.arkv_check()
+        res.append((torch.stack(outs), [gpu.arkv_export_unit(b, l, h) for b in range(2) for l in range(3)
+                                        for h in range(4)]))
+    torch.testing.assert_close(res[0][0], res[1][0], rtol=RTOL, atol=ATOL)
+    for e2, e3 in zip(res[0][1], res[1][1]):
+        for key in ("state", "q_k", "k_scale", "o_k", "o_v"):
+            np.testing.assert_array_equal(e2[key], e3[key])
+
+
 def test_batch_and_spare_waves():
     """Batch 3 with only 2 staging slots: every tailor runs in several waves."""
     sh = Shape(batch=3, n_layers=2, n_q_heads=4, n_kv_heads=2, head_dim=32, prompt_len=200, window=8)
