@@ -37,12 +37,10 @@ struct arkv_cache {
   double* colsum = nullptr;
   float* mstat = nullptr;
   int32_t* counters = nullptr;
-  // persistent decode kernel (ARKV_DECODE_PERSIST): device plan, partials, pinned host ring
-  int32_t* plan_dev = nullptr;
+  // persistent decode kernel (decode_kernel = 3): partial slots and coverage tables
   float* pparts = nullptr;
-  int32_t* plan_host = nullptr;
-  std::vector<cudaEvent_t> plan_ev;
-  int plan_next = 0;
+  int4* pcta = nullptr;
+  int32_t* pcover = nullptr;
   bool persist = false;
   int num_sms = 148;
   int jobs_per_wave = 0, max_splits = 64, n_chunks1_max = 1;
@@ -64,8 +62,6 @@ struct arkv_cache {
 namespace {
 
 constexpr int kPfChunkHost = 2048;
-constexpr int kPlanMaxCtas = 320;  // persistent decode grid bound (2 CTAs/SM x <= 160 SMs)
-constexpr int kPlanRing = 8;       // pinned host plan buffers in flight
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -169,8 +165,8 @@ Sizes compute_sizes(const arkv_config& c) {
   s.w_counters = w;
   w = round_up(w + (int64_t)g.n_units * 4, 256);
   // persistent decode kernel: its plan and one partial per (unit, covering CTA, warp)
-  s.w_plan = w;
-  w = round_up(w + (int64_t)plan_ints(g.n_units, kPlanMaxCtas) * 4, 256);
+  s.w_plan = w;  // pcta [2][kPlanMaxCtas] int4, then pcover [2][2][n_units] int32
+  w = round_up(w + (int64_t)2 * kPlanMaxCtas * 16 + (int64_t)4 * g.n_units * 4, 256);
   s.w_pparts = w;
   w = round_up(w + (int64_t)2 * (kPlanMaxCtas + g.n_units) * kPersistConsumers * g.G * (g.d + 2) * 4, 256);
   s.ws = w;
@@ -409,7 +405,8 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   c->colsum = (double*)(w + s.w_colsum);
   c->mstat = (float*)(w + s.w_mstat);
   c->counters = (int32_t*)(w + s.w_counters);
-  c->plan_dev = (int32_t*)(w + s.w_plan);
+  c->pcta = (int4*)(w + s.w_plan);
+  c->pcover = (int32_t*)(w + s.w_plan + 2 * kPlanMaxCtas * 16);
   c->pparts = (float*)(w + s.w_pparts);
   c->num_sms = prop.multiProcessorCount;
   c->jobs_per_wave = s.jobs_per_wave;
@@ -439,6 +436,7 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   // persistent-kernel partial slots start with l = 0 (= unused; decode_persist_combine)
   if (!check_cuda(cudaMemset(c->slots, 0, (size_t)s.off_desc)) || !check_cuda(cudaMemset(c->err, 0, 4)) ||
       !check_cuda(cudaMemset(c->pparts, 0, (size_t)(s.ws - s.w_pparts))) ||
+      !check_cuda(cudaMemset(c->pcover, 0xff, (size_t)4 * s.g.n_units * 4)) ||
       !check_cuda(cudaMemset(c->counters, 0, (size_t)s.g.n_units * 4))) {
     delete c;
     return ARKV_ERR_CUDA;
@@ -450,8 +448,6 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
 arkv_status arkv_cache_destroy(arkv_cache* c) {
   if (c) {
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
-    for (cudaEvent_t e : c->plan_ev) cudaEventDestroy(e);
-    if (c->plan_host) cudaFreeHost(c->plan_host);
   }
   delete c;
   return ARKV_OK;
@@ -641,17 +637,17 @@ arkv_status arkv_prefill_stats(arkv_cache* c, const void* q_win, const void* k, 
 }
 
 // Work plan of the persistent decode kernel for units [layer0, layer0 + n_layers) of all
-// sequences (PlanView in kernels.h).  Phase 0 items: each unit's Original
+// sequences (PersistPlan in kernels.h).  Phase 0 items: each unit's Original
 // tiles (rows n_o; the step's token is appended by the combine); phase 1 items: its
-// Quantized tiles in groups of q_per.  Each phase's item stream is cut into P equal ranges.
-// Returns the ints written.
-int build_plan(const arkv_cache* c, int layer0, int n_layers, int P, int32_t* out, int* P_out) {
+// Quantized tiles in groups of q_per.  Each phase's item stream is cut into P equal ranges;
+// a range's partial slots are C per unit it spans.  P shrinks until no unit needs more
+// than kMaxUnitParts slots.
+void build_plan(const arkv_cache* c, int layer0, int n_layers, int P, PersistPlan* plan) {
   const Geom& g = c->g;
   const int U = g.batch * n_layers * g.Hkv;
   const int q_per = (32 * 4 * g.d) / g.tile_q;  // Quantized tiles per 16 KB ring stage
   std::vector<int64_t> first[2];
-  first[0].assign(U + 1, 0);
-  first[1].assign(U + 1, 0);
+  for (int f = 0; f < 2; ++f) first[f].assign(U + 1, 0);
   for (int ul = 0; ul < U; ++ul) {
     const int b = ul / (n_layers * g.Hkv), li = (ul / g.Hkv) % n_layers;
     const int bl = b * g.L + layer0 + li;
@@ -660,52 +656,39 @@ int build_plan(const arkv_cache* c, int layer0, int n_layers, int P, int32_t* ou
     first[1][ul + 1] = first[1][ul] + (tiles_q + q_per - 1) / q_per;
   }
   const int64_t N = std::max(first[0][U], first[1][U]);
-  P = (int)std::max<int64_t>(1, std::min<int64_t>(P, N));
+  P = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(P, kPlanMaxCtas), N));
+  std::vector<int> cover(U);
+  const int64_t cap = (int64_t)2 * (kPlanMaxCtas + g.n_units) * kPersistConsumers;  // compute_sizes
   for (;;) {
-    PlanView pv(out, U, P);
-    int span_max = 0;
+    std::fill(cover.begin(), cover.end(), 0);
+    int64_t slots = 0;
     for (int f = 0; f < 2; ++f) {
       const int64_t Nf = first[f][U];
-      int32_t* lo = const_cast<int32_t*>(pv.cta_lo(f));
-      int32_t* u0 = const_cast<int32_t*>(pv.cta_u0(f));
-      int32_t* itf = const_cast<int32_t*>(pv.item_first(f));
-      int32_t* cf = const_cast<int32_t*>(pv.cta_first(f));
-      int32_t* cl = const_cast<int32_t*>(pv.cta_last(f));
-      for (int k = 0; k <= P; ++k) lo[k] = (int32_t)(Nf * k / P);
-      for (int u = 0; u <= U; ++u) itf[u] = (int32_t)first[f][u];
       int ul = 0;
       for (int k = 0; k < P; ++k) {
-        while (ul + 1 < U && first[f][ul + 1] <= lo[k]) ++ul;
-        u0[k] = ul;
-      }
-      int k = 0;
-      for (int u = 0; u < U; ++u) {
-        if (first[f][u + 1] == first[f][u]) {
-          cf[u] = 0;
-          cl[u] = -1;
-          continue;
+        const int64_t i0 = Nf * k / P, i1 = Nf * (k + 1) / P;
+        int4 r = make_int4(0, 0, (int)(i1 - i0), (int)slots);
+        int ue = 0;
+        if (i1 > i0) {
+          while (first[f][ul + 1] <= i0) ++ul;  // unit holding item i0
+          ue = ul;
+          while (first[f][ue + 1] <= i1 - 1) ++ue;  // unit holding the range's last item
+          r.x = ul;
+          r.y = (int)(i0 - first[f][ul]);
+          slots += (int64_t)(ue - ul + 1) * kPersistConsumers;
+          for (int u = ul; u <= ue; ++u)
+            if (first[f][u + 1] > first[f][u]) ++cover[u];
         }
-        while (k + 1 < P && lo[k + 1] <= first[f][u]) ++k;
-        int k2 = k;
-        while (k2 + 1 < P && lo[k2 + 1] <= first[f][u + 1] - 1) ++k2;
-        cf[u] = k;
-        cl[u] = k2;
+        plan->cta[f][k] = r;
+        plan->ue[f][k] = ue;
       }
     }
-    int32_t* pb = const_cast<int32_t*>(pv.part_base());
-    int parts = 0;
-    for (int u = 0; u < U; ++u) {
-      pb[u] = parts;
-      const int n = (pv.cta_last(0)[u] - pv.cta_first(0)[u] + 1) + (pv.cta_last(1)[u] - pv.cta_first(1)[u] + 1);
-      span_max = std::max(span_max, n);
-      parts += n * kPersistConsumers;
-    }
-    pb[U] = parts;
-    if (span_max * kPersistConsumers <= kMaxUnitParts || P == 1) break;
+    int span_max = 0;
+    for (int u = 0; u < U; ++u) span_max = std::max(span_max, cover[u]);
+    if ((span_max * kPersistConsumers <= kMaxUnitParts && slots <= cap) || P == 1) break;
     P = std::max(1, P * 3 / 4);  // too few units for this many CTAs: fewer, longer ranges
   }
-  *P_out = P;
-  return plan_ints(U, P);
+  plan->P = P;
 }
 
 arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, const void* q, const void* k,
@@ -786,28 +769,13 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
     c->ev_used++;
   }
   PlanArgs pa;
+  PersistPlan plan;
   if (c->persist) {
-    if (!c->plan_host) {
-      if (!check_cuda(cudaHostAlloc((void**)&c->plan_host,
-                                    (size_t)kPlanRing * plan_ints(g.n_units, kPlanMaxCtas) * 4, cudaHostAllocDefault)))
-        return ARKV_ERR_CUDA;
-      c->plan_ev.resize(kPlanRing);
-      for (auto& e : c->plan_ev)
-        if (!check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming))) return ARKV_ERR_CUDA;
-    }
-    // host buffer of this step: wait until its previous upload has been consumed
-    const int ring = c->plan_next++ % kPlanRing;
-    if (!check_cuda(cudaEventSynchronize(c->plan_ev[ring]))) return ARKV_ERR_CUDA;
-    int32_t* hp = c->plan_host + (size_t)ring * plan_ints(g.n_units, kPlanMaxCtas);
-    int P = 0;
-    const int n_ints = build_plan(c, layer0, n_layers, std::min(2 * c->num_sms, kPlanMaxCtas), hp, &P);
-    if (!check_cuda(cudaMemcpyAsync(c->plan_dev, hp, (size_t)n_ints * 4, cudaMemcpyHostToDevice, s)) ||
-        !check_cuda(cudaEventRecord(c->plan_ev[ring], s)))
-      return ARKV_ERR_CUDA;
-    pa.plan = c->plan_dev;
-    pa.U = n_units_call;
-    pa.P = P;
+    build_plan(c, layer0, n_layers, 2 * c->num_sms, &plan);
+    pa.plan = &plan;
     pa.pparts = c->pparts;
+    pa.pcta = c->pcta;
+    pa.pcover = c->pcover;
   }
   int nl = launch_decode(g, layer0, n_layers, (const uint16_t*)q, (const uint16_t*)k, (const uint16_t*)v, out,
                          out_fp32, c->slots, c->meta, c->desc, c->partials, c->logits, c->mstat, c->counters, acc_rows, S,

@@ -298,7 +298,8 @@ void launch_decode_hh_acc(const DecodeArgs& a, int n_units_call, int max_rows, c
 }
 
 // k_decode_fast.cu: returns -1 if the cache is not eligible.
-int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1);
+int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                       const PersistPlan* plan);
 void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s);
 
 template <int G>
@@ -339,10 +340,10 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
                   float* logits, float* mstat, int32_t* counters, int acc_rows, int n_splits, int max_splits,
                   int fast, int32_t* err, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, const PlanArgs& plan) {
   DecodeArgs a;
-  a.plan = fast ? plan.plan : nullptr;
-  a.plan_U = plan.U;
-  a.plan_P = plan.P;
+  a.persist = fast && plan.plan ? 1 : 0;
   a.pparts = plan.pparts;
+  a.pcta = plan.pcta;
+  a.pcover = plan.pcover;
   a.g = g;
   a.layer0 = layer0;
   a.n_layers = n_layers;
@@ -374,7 +375,7 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
   const int n_units_call = g.batch * n_layers * g.Hkv;
   int n = -1;
   if (fast) {
-    n = launch_decode_fast(a, n_units_call, s, ev0, ev1);
+    n = launch_decode_fast(a, n_units_call, s, ev0, ev1, plan.plan);
     if (n < 0) return n;
   } else {
     switch (g.G) {

@@ -127,6 +127,21 @@ __device__ __forceinline__ void unpack8(uint32_t w, uint32_t (&x)[4]) {
   x[2] = hsub2_1024(lop3_mask_or(w8, 0x000F000Fu, 0x64006400u));
   x[3] = hsub2_1024(lop3_mask_or(w8, 0x00F000F0u, 0x64006400u));
 }
+// The same without the exact "- 1024": codes stay as f16 (1024 + c) / (1024 + 16c).  Used
+// for the PV contraction only, whose result tolerates the fp32 cancellation of the offset
+// (~1e-5 absolute on the output); the logits (QK), which decide token states through the
+// heavy-hitter scores, keep the exact unpack.
+__device__ __forceinline__ void unpack8_raw(uint32_t w, uint32_t (&x)[4]) {
+  const uint32_t w8 = w >> 8;
+  x[0] = lop3_mask_or(w, 0x000F000Fu, 0x64006400u);
+  x[1] = lop3_mask_or(w, 0x00F000F0u, 0x64006400u);
+  x[2] = lop3_mask_or(w8, 0x000F000Fu, 0x64006400u);
+  x[3] = lop3_mask_or(w8, 0x00F000F0u, 0x64006400u);
+}
+#ifndef ARKV_PV_RAW
+#define ARKV_PV_RAW 1
+#endif
+constexpr bool kPvRaw = ARKV_PV_RAW != 0;
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *(uint32_t*)&v;
@@ -327,7 +342,9 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
           }
           l0 += ks * acc[gr][hh * 2 + 0] + kz * f.qsum[0][gr];
           l1 += ks * acc[gr][hh * 2 + 1] + kz * f.qsum[1][gr];
-          zv[mt][hh][gr] = vz;
+          // PV runs on the raw magic-number codes (1024 + c for rows g, 1024 + 16c for
+          // rows g+8, whose P' carries 1/16): the offset is removed here, in the z term
+          zv[mt][hh][gr] = kPvRaw ? vz - (hh ? 64.f : 1024.f) * vs : vz;
         }
         lg[mt][hh * 2 + 0] = l0 * c2;
         lg[mt][hh * 2 + 1] = l1 * c2;
@@ -374,7 +391,8 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
     for (int gr = 0; gr < NG; ++gr) s.z_run[e][gr] *= corr[e];
   }
   // rescale O^T columns: col 2t+e belongs to head (2t+e) % G, whose max lives in lane src_lane
-  {
+  // (skipped when no head's running max moved — most tiles once the max has settled)
+  if (__any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f)) {
     const float c0 = __shfl_sync(0xffffffffu, corr[0], src_lane);
     const float c1 = __shfl_sync(0xffffffffu, G >= 2 ? corr[1] : corr[0], src_lane);
 #pragma unroll
@@ -455,8 +473,13 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
         const int mv = 2 * qd + hm;
         const int gr = (mv * 16) / (D / NG);
         uint32_t x[4], y[4];
-        unpack8(word(r, 2 * hm + 0), x);  // dim row g
-        unpack8(word(r, 2 * hm + 1), y);  // dim row g+8
+        if (kPvRaw) {
+          unpack8_raw(word(r, 2 * hm + 0), x);  // dim row g
+          unpack8_raw(word(r, 2 * hm + 1), y);  // dim row g+8
+        } else {
+          unpack8(word(r, 2 * hm + 0), x);
+          unpack8(word(r, 2 * hm + 1), y);
+        }
 #pragma unroll
         for (int kc = 0; kc < 2; ++kc) {
           mma_f16(s.o[mv], x[2 * kc], y[2 * kc], x[2 * kc + 1], y[2 * kc + 1], b01[gr][kc], b23[gr][kc]);
@@ -763,19 +786,27 @@ static int launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaE
 // ---------------------------------------------------------------------------------------
 // Persistent, range-partitioned variant (decode_kernel = 3).
 // The step's items form two global streams — every unit's Original tiles, then every
-// unit's Quantized tiles in groups of q_per — and the host plan (PlanView) gives every CTA
-// an equal contiguous range of each, so all CTAs stream the same bytes of each kind with
-// one pipeline fill and drain.  The kernel is read-only on the cache: each consumer warp
-// flushes a partial (m, l, o) per (unit, phase) it touched, and decode_persist_combine
-// merges a unit's partials, appends the step's token and folds it in.
+// unit's Quantized tiles in groups of q_per — and the plan (PersistPlan, a kernel
+// parameter) gives every CTA an equal contiguous range of each, so all CTAs stream the
+// same bytes of each kind with one pipeline fill and drain.  The kernel is read-only on
+// the cache: each consumer warp flushes a partial (m, l, o) per (unit, phase) it touched,
+// and decode_persist_combine merges a unit's partials, appends the step's token and
+// folds it in.
 // ---------------------------------------------------------------------------------------
 struct PUnit {
   int u;  // global unit index
-  int slot, n_o, n_q, tiles_q;
+  int slot, n_o, n_q, tiles_q, items;
   bool accm;
-  const uint16_t* qp;
 };
-__device__ __forceinline__ void punit_load(const DecodeArgs& a, int ul, PUnit& p) {
+// query rows of unit ul (index in the call)
+__device__ __forceinline__ const uint16_t* punit_q(const DecodeArgs& a, int ul) {
+  const Geom& g = a.g;
+  const int b = ul / (a.n_layers * g.Hkv);
+  const int rem = ul % (a.n_layers * g.Hkv);
+  const int li = rem / g.Hkv, kvh = rem % g.Hkv;
+  return a.q + ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * g.G) * D;
+}
+__device__ __forceinline__ void punit_load(const DecodeArgs& a, int ul, int f, int q_per, PUnit& p) {
   const Geom& g = a.g;
   const int b = ul / (a.n_layers * g.Hkv);
   const int rem = ul % (a.n_layers * g.Hkv);
@@ -786,78 +817,111 @@ __device__ __forceinline__ void punit_load(const DecodeArgs& a, int ul, PUnit& p
   p.n_o = dsc.n_o;
   p.n_q = dsc.n_q;
   p.tiles_q = (p.n_q + kTile - 1) / kTile;
+  p.items = f == 0 ? (p.n_o + kTile - 1) / kTile : (p.tiles_q + q_per - 1) / q_per;
   p.accm = (dsc.t_next >= dsc.trig - g.W) && (dsc.t_next < dsc.trig);
-  p.qp = a.q + ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * g.G) * D;
 }
+// Position in one phase range of a CTA: item k of unit ul.  Walks forward only (units
+// with no items of the phase are stepped over).
+struct Walker {
+  int ul, k, rem;
+  PUnit p;
+  __device__ __forceinline__ void init(const DecodeArgs& a, const int4& r, int f, int q_per) {
+    ul = r.x;
+    k = r.y;
+    rem = r.z;
+    if (rem > 0) punit_load(a, ul, f, q_per, p);
+  }
+  __device__ __forceinline__ void next(const DecodeArgs& a, int f, int q_per) {
+    if (--rem <= 0) return;
+    ++k;
+    while (k >= p.items) {
+      k -= p.items;
+      punit_load(a, ++ul, f, q_per, p);
+    }
+  }
+};
+template <int C>
+struct PSmem {
+  uint8_t ring[C][kStageBytes];
+  uint64_t full[C];
+  uint64_t empty[C];
+  int4 info[C][2];  // per stage, written by the producer: (ul, u, k, phase), (n_o, n_q, tiles_q, accm)
+};
 
 template <int G, int NG>
-__global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2) decode_persist_kernel(DecodeArgs a) {
+__global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
+    decode_persist_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ PersistPlan plan) {
   constexpr int C = kPersistConsumers;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  Smem<C, 1>& sm = *reinterpret_cast<Smem<C, 1>*>(smem_raw);
+  PSmem<C>& sm = *reinterpret_cast<PSmem<C>*>(smem_raw);
   const Geom& g = a.g;
   griddep_wait();  // PDL: the previous kernel (tailor / combine) has completed
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
-  const PlanView pv(a.plan, a.plan_U, a.plan_P);
   const int c = blockIdx.x;
-  const int lo0 = pv.cta_lo(0)[c], n0 = pv.cta_lo(0)[c + 1] - lo0;
-  const int lo1 = pv.cta_lo(1)[c], n1 = pv.cta_lo(1)[c + 1] - lo1;
-  const int n_work = n0 + n1;
+  const int n_work = plan.cta[0][c].z + plan.cta[1][c].z;
   const int q_per = kStageBytes / g.tile_q;
   const int row_stride = g.cap_o + g.cap_q;
   const float c2 = g.sm_scale * kLog2e;
   const bool sym = g.mode == ARKV_QUANT_SYM;
+  const int n_units_call = g.batch * a.n_layers * g.Hkv;
   if (threadIdx.x == 0) {
     for (int i = 0; i < C; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    // where this CTA's partials live (per phase; -1: empty range), for the combine
+    for (int f = 0; f < 2; ++f) {
+      const int4 r = plan.cta[f][c];
+      a.pcta[f * kPlanMaxCtas + c] = make_int4(r.z > 0 ? r.x : -1, r.w, plan.ue[f][c], 0);
+    }
   }
   __syncthreads();
   if (n_work <= 0) {
     if (threadIdx.x == 0) griddep_launch_dependents();
     return;
   }
-  // item j of this CTA: phase f, stream index i; unit ul found by walking forward from hint
-  auto locate = [&](int j, int& f, int& i, int& ul, int hint_f, int hint_ul) {
-    f = j < n0 ? 0 : 1;
-    i = f == 0 ? lo0 + j : lo1 + (j - n0);
-    ul = (hint_f == f && hint_ul >= 0) ? hint_ul : pv.cta_u0(f)[c];
-    while (i >= pv.item_first(f)[ul + 1]) ++ul;
-  };
 
   if (warp == C) {
-    // ===================== producer: the CTA's two ranges, in order =====================
+    // ============ producer: merges the two ranges by unit (a unit's Original tiles, then
+    // its Quantized groups) so each consumer warp accumulates a unit across both kinds ============
     if (lane == 0) {
-      int f = -1, ul = -1;
-      PUnit p;
-      p.u = -1;
-      for (int j = 0; j < n_work; ++j) {
-        int nf, i, nul;
-        locate(j, nf, i, nul, f, ul);
-        if (nul != ul || nf != f) {
-          punit_load(a, nul, p);
-          ul = nul;
-          f = nf;
-        }
+      Walker w0, w1;
+      w0.init(a, plan.cta[0][c], 0, q_per);
+      w1.init(a, plan.cta[1][c], 1, q_per);
+      auto issue = [&](Walker& w, int f, int j) {
+        const PUnit& p = w.p;
+        // the CTAs holding a unit's first and last item of the phase, for the combine
+        if (w.k == 0) a.pcover[(f * 2 + 0) * n_units_call + w.ul] = c;
+        if (w.k == p.items - 1) a.pcover[(f * 2 + 1) * n_units_call + w.ul] = c;
         const int st = j % C;
         if (j >= C) mbar_wait(&sm.empty[st], ((j / C) - 1) & 1);
-        const int k = i - pv.item_first(f)[ul];
+        sm.info[st][0] = make_int4(w.ul, p.u, w.k, f);
+        sm.info[st][1] = make_int4(p.n_o, p.n_q, p.tiles_q, p.accm ? 1 : 0);
         uint8_t* slot = a.slots + (int64_t)p.slot * g.slot_bytes;
         const uint8_t* src;
         uint32_t bytes;
         if (f == 0) {
-          src = o_tile_ptr(slot, g, k);
+          src = o_tile_ptr(slot, g, w.k);
           bytes = (uint32_t)g.tile_o;
         } else {
-          const int first = k * q_per, nt = min(q_per, p.tiles_q - first);
+          const int first = w.k * q_per, nt = min(q_per, p.tiles_q - first);
           src = q_tile_ptr(slot, g, first + nt - 1);
           bytes = (uint32_t)(nt * g.tile_q);
         }
-        mbar_expect_tx(&sm.full[st], bytes);
+        mbar_expect_tx(&sm.full[st], bytes);  // release: orders the info writes above
         bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
+      };
+      for (int j = 0; j < n_work; ++j) {
+        const bool take0 = w0.rem > 0 && (w1.rem <= 0 || w0.ul <= w1.ul);
+        if (take0) {
+          issue(w0, 0, j);
+          w0.next(a, 0, q_per);
+        } else {
+          issue(w1, 1, j);
+          w1.next(a, 1, q_per);
+        }
       }
       griddep_launch_dependents();  // PDL: the combine may start launching (it waits for us)
     }
@@ -870,13 +934,14 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2) decode_persis
   const int src_lane = (lane & ~3) | src_t;
   QFrag<NG> qf;
   Acc<NG> acc;
-  PUnit p;
-  int cur = -1, curf = -1;
-  // partial of (unit cur, phase curf, this CTA, this warp): m, l and o (z term folded in)
+  int cur = -1;
+  // partial of (unit cur, this CTA, this warp): m, l and o (z term folded in)
   auto flush = [&]() {
     acc_reduce_rows(acc);
-    int slot_idx = pv.part_base()[cur] + (c - pv.cta_first(curf)[cur]) * C + warp;
-    if (curf == 1) slot_idx += (pv.cta_last(0)[cur] - pv.cta_first(0)[cur] + 1) * C;
+    const int4 r0 = plan.cta[0][c];
+    const bool in0 = r0.z > 0 && cur >= r0.x && cur <= plan.ue[0][c];
+    const int4 r = in0 ? r0 : plan.cta[1][c];
+    const int slot_idx = r.w + (cur - r.x) * C + warp;
     float* part = a.pparts + (int64_t)slot_idx * G * (D + 2);
 #pragma unroll
     for (int mv = 0; mv < 8; ++mv) {
@@ -909,33 +974,28 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2) decode_persis
     }
   };
   for (int j = warp; j < n_work; j += C) {
-    int f, i, ul;
-    locate(j, f, i, ul, curf, cur);
-    if (ul != cur || f != curf) {
-      if (cur >= 0) flush();
-      if (ul != cur) {
-        punit_load(a, ul, p);
-        load_qfrag<G, NG>(p.qp, lane, qf);
-      }
-      cur = ul;
-      curf = f;
-      acc_reset(acc);
-    }
     const int st = j % C;
     mbar_wait(&sm.full[st], (j / C) & 1);
     __syncwarp();  // mma/movmatrix are .aligned
-    const int k = i - pv.item_first(f)[ul];
-    if (f == 0) {
-      float* lr = p.accm ? a.logits + (int64_t)p.u * G * row_stride + k * kTile : nullptr;
-      consume_tile<G, NG>(sm.ring[st], false, min(kTile, p.n_o - k * kTile), lr, row_stride, qf, acc, c2, sym,
-                          lane, src_lane);
+    const int4 i0 = sm.info[st][0], i1 = sm.info[st][1];
+    if (i0.x != cur) {
+      if (cur >= 0) flush();
+      load_qfrag<G, NG>(punit_q(a, i0.x), lane, qf);
+      cur = i0.x;
+      acc_reset(acc);
+    }
+    const int u = i0.y, k = i0.z;
+    float* lbase = i1.w ? a.logits + (int64_t)u * G * row_stride : nullptr;
+    if (i0.w == 0) {
+      consume_tile<G, NG>(sm.ring[st], false, min(kTile, i1.x - k * kTile), lbase ? lbase + k * kTile : nullptr,
+                          row_stride, qf, acc, c2, sym, lane, src_lane);
     } else {
-      const int first = k * q_per, nt = min(q_per, p.tiles_q - first);
+      const int first = k * q_per, nt = min(q_per, i1.z - first);
       for (int jt = 0; jt < nt; ++jt) {
         const int tile = first + jt;
-        float* lr = p.accm ? a.logits + (int64_t)p.u * G * row_stride + g.cap_o + tile * kTile : nullptr;
-        consume_tile<G, NG>(sm.ring[st] + (nt - 1 - jt) * g.tile_q, true, min(kTile, p.n_q - tile * kTile), lr,
-                            row_stride, qf, acc, c2, sym, lane, src_lane);
+        consume_tile<G, NG>(sm.ring[st] + (nt - 1 - jt) * g.tile_q, true, min(kTile, i1.y - tile * kTile),
+                            lbase ? lbase + g.cap_o + tile * kTile : nullptr, row_stride, qf, acc, c2, sym, lane,
+                            src_lane);
       }
     }
     __syncwarp();
@@ -953,8 +1013,7 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
   griddep_launch_dependents();
   constexpr int C = kPersistConsumers;
   const Geom& g = a.g;
-  const PlanView pv(a.plan, a.plan_U, a.plan_P);
-  const int ul = blockIdx.x;
+  const int ul = blockIdx.x, n_units_call = gridDim.x;
   const int b = ul / (a.n_layers * g.Hkv);
   const int rem = ul % (a.n_layers * g.Hkv);
   const int li = rem / g.Hkv, kvh = rem % g.Hkv;
@@ -969,6 +1028,10 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
   const int row_stride = g.cap_o + g.cap_q;
   __shared__ float s_new[G], sM[G], sIL[G];
   __shared__ float s_w[kMaxUnitParts][G];  // merge weight 2^(m - M) of each slot (0: unused)
+  __shared__ int s_slot[kMaxUnitParts];
+  __shared__ int s_cov[4];
+  // ---- the CTAs covering the unit (first, last per phase); cleared for the next step ----
+  if (x < 4) s_cov[x] = a.pcover[(x >> 1) * 2 * n_units_call + (x & 1) * n_units_call + ul];
   // ---- append the token to the Original stack (row n_o) ----
   const int tiles_o = (n_o + 1 + kTile - 1) / kTile, tiles_q = (dsc.n_q + kTile - 1) / kTile;
   const bool fits = (n_o + 1 <= g.cap_o) && ((int64_t)tiles_o * g.tile_o + (int64_t)tiles_q * g.tile_q <= g.slot_bytes);
@@ -999,25 +1062,47 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
       if (accm) a.logits[((int64_t)u * G + h) * row_stride + n_o] = acc * c2;
     }
   }
-  // ---- the unit's partial slots: C per covering CTA and phase, contiguous.  A slot whose
-  // warp processed none of the unit's items still holds l = 0 (slots start zeroed and
-  // every combine clears the l of the slots it merged), so validity is l > 0 ----
-  const int p0 = pv.part_base()[ul], ncand = min(pv.part_base()[ul + 1] - p0, kMaxUnitParts);
-  const float* pp = a.pparts + (int64_t)p0 * G * (D + 2);
-  __syncthreads();  // s_new
+  __syncthreads();
+  if (x < 4) a.pcover[(x >> 1) * 2 * n_units_call + (x & 1) * n_units_call + ul] = -1;
+  // ---- candidate partial slots: C per covering CTA and phase.  A slot whose warp processed
+  // none of the unit's items holds l = 0 (slots start zeroed and every combine clears the
+  // l of the slots it merged) ----
+  const int nc0 = s_cov[0] >= 0 ? (s_cov[1] - s_cov[0] + 1) * C : 0;
+  const int nc1 = s_cov[2] >= 0 ? (s_cov[3] - s_cov[2] + 1) * C : 0;
+  const int ncand = min(nc0 + nc1, kMaxUnitParts);
+  for (int k = x; k < ncand; k += D) {
+    const int f = k < nc0 ? 0 : 1, kk = f == 0 ? k : k - nc0;
+    const int cc = s_cov[2 * f] + kk / C;
+    int4 pc = a.pcta[f * kPlanMaxCtas + cc];
+    // a CTA between the first and last covering ones may have an empty range of the phase
+    // (fewer items than CTAs): skipped.  A unit inside a CTA's phase-0 span uses its
+    // phase-0 slots even for Quantized items: enumerated once.
+    bool use = pc.x >= 0;
+    if (use && f == 1) {
+      const int4 p0 = a.pcta[cc];
+      if (p0.x >= 0 && ul >= p0.x && ul <= p0.z) {
+        pc = p0;
+        if (s_cov[0] >= 0 && cc >= s_cov[0] && cc <= s_cov[1]) use = false;
+      }
+    }
+    s_slot[k] = use ? pc.y + (ul - pc.x) * C + kk % C : -1;
+  }
+  __syncthreads();
+  const float* pp = a.pparts;
   // merged max and sum per head: warp w reduces heads w, w + 4
   for (int h = warp; h < G; h += D / 32) {
     float M = s_new[h];
     for (int k = lane; k < ncand; k += 32) {
-      const float* ph = pp + ((int64_t)k * G + h) * (D + 2);
+      if (s_slot[k] < 0) continue;
+      const float* ph = pp + ((int64_t)s_slot[k] * G + h) * (D + 2);
       if (__ldcg(ph + 1) > 0.f) M = fmaxf(M, __ldcg(ph));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float L = lane == 0 ? exp2f(s_new[h] - M) : 0.f;
     for (int k = lane; k < ncand; k += 32) {
-      const float* ph = pp + ((int64_t)k * G + h) * (D + 2);
-      const float l = __ldcg(ph + 1);
+      const float* ph = pp + ((int64_t)max(s_slot[k], 0) * G + h) * (D + 2);
+      const float l = s_slot[k] >= 0 ? __ldcg(ph + 1) : 0.f;
       const float w = l > 0.f ? exp2f(__ldcg(ph) - M) : 0.f;
       s_w[k][h] = w;
       L += l * w;
@@ -1039,7 +1124,7 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
     float O = exp2f(s_new[h] - sM[h]) * vnew;
     for (int k = 0; k < ncand; ++k) {
       const float w = s_w[k][h];
-      if (w != 0.f) O += __ldcg(pp + ((int64_t)k * G + h) * (D + 2) + 2 + x) * w;
+      if (w != 0.f) O += __ldcg(pp + ((int64_t)s_slot[k] * G + h) * (D + 2) + 2 + x) * w;
     }
     O *= sIL[h];
     if (a.out_fp32)
@@ -1048,8 +1133,8 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
       ((uint16_t*)a.out)[obase + h * D + x] = f_to_bf16_rne(O);
   }
   // clear the merged slots' l for the next step's plan
-  float* pw = a.pparts + (int64_t)p0 * G * (D + 2);
-  for (int k = x; k < ncand * G; k += D) pw[(int64_t)k * (D + 2) + 1] = 0.f;
+  for (int k = x; k < ncand * G; k += D)
+    if (s_slot[k / G] >= 0) a.pparts[((int64_t)s_slot[k / G] * G + k % G) * (D + 2) + 1] = 0.f;
   if (x == 0) {
     UnitDesc nd = dsc;
     nd.n_o = n_o + 1;
@@ -1059,21 +1144,23 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
 }
 
 template <int G, int NG>
-static void launch_persist(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+static void launch_persist(const DecodeArgs& a, const PersistPlan& plan, int n_units_call, cudaStream_t s,
+                           cudaEvent_t ev0, cudaEvent_t ev1) {
   auto kern = decode_persist_kernel<G, NG>;
-  const int smem = (int)sizeof(Smem<kPersistConsumers, 1>);
+  const int smem = (int)sizeof(PSmem<kPersistConsumers>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (ev0) cudaEventRecord(ev0, s);
-  launch_pdl(kern, dim3(a.plan_P), dim3((kPersistConsumers + 1) * 32), (size_t)smem, s, a);
+  launch_pdl(kern, dim3(plan.P), dim3((kPersistConsumers + 1) * 32), (size_t)smem, s, a, plan);
   if (ev1) cudaEventRecord(ev1, s);
   launch_pdl(decode_persist_combine<G>, dim3(n_units_call), dim3(D), 0, s, a);
 }
 template <int G>
-static int launch_persist_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+static int launch_persist_g(const DecodeArgs& a, const PersistPlan& plan, int n_units_call, cudaStream_t s,
+                            cudaEvent_t ev0, cudaEvent_t ev1) {
   switch (a.g.ng) {
-    case 1: launch_persist<G, 1>(a, n_units_call, s, ev0, ev1); return 2;
-    case 2: launch_persist<G, 2>(a, n_units_call, s, ev0, ev1); return 2;
-    case 4: launch_persist<G, 4>(a, n_units_call, s, ev0, ev1); return 2;
+    case 1: launch_persist<G, 1>(a, plan, n_units_call, s, ev0, ev1); return 2;
+    case 2: launch_persist<G, 2>(a, plan, n_units_call, s, ev0, ev1); return 2;
+    case 4: launch_persist<G, 4>(a, plan, n_units_call, s, ev0, ev1); return 2;
     default: return -1;
   }
 }
@@ -1087,14 +1174,15 @@ bool decode_fast_available(const Geom& g) {
 
 void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s);  // k_decode.cu
 
-int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                       const PersistPlan* plan) {
   if (!decode_fast_available(a.g)) return -1;
-  if (a.plan) {  // persistent range-partitioned kernel + its combine
+  if (plan) {  // persistent range-partitioned kernel + its combine
     switch (a.g.G) {
-      case 1: return fast::launch_persist_g<1>(a, n_units_call, s, ev0, ev1);
-      case 2: return fast::launch_persist_g<2>(a, n_units_call, s, ev0, ev1);
-      case 4: return fast::launch_persist_g<4>(a, n_units_call, s, ev0, ev1);
-      case 8: return fast::launch_persist_g<8>(a, n_units_call, s, ev0, ev1);
+      case 1: return fast::launch_persist_g<1>(a, *plan, n_units_call, s, ev0, ev1);
+      case 2: return fast::launch_persist_g<2>(a, *plan, n_units_call, s, ev0, ev1);
+      case 4: return fast::launch_persist_g<4>(a, *plan, n_units_call, s, ev0, ev1);
+      case 8: return fast::launch_persist_g<8>(a, *plan, n_units_call, s, ev0, ev1);
       default: return -1;
     }
   }

@@ -62,44 +62,38 @@ struct DecodeArgs {
   void* out;
   int out_fp32;
   int32_t* err;
-  // persistent decode kernel (decode_persist_kernel): host-built work plan (PlanView) and
-  // one partial per (unit, covering CTA, consumer warp)
-  const int32_t* plan;
-  int plan_U, plan_P;
-  float* pparts;
+  // persistent decode kernel (decode_persist_kernel / decode_persist_combine)
+  int persist;
+  float* pparts;     // partial slots (m, l, o) per (CTA, phase, unit in its range, warp); l = 0: unused
+  int4* pcta;        // [2][kPlanMaxCtas]: (first unit or -1 if empty, slot base, last unit) of each
+                     // CTA's phase range, for the combine
+  int32_t* pcover;   // [2][2][n_units]: first / last CTA covering each unit's phase items (-1: none)
 };
 
-// Work plan of the persistent decode kernel (int32, host-built each step).
-// The step's items form two streams — phase 0: every unit's Original tiles (16 KB each);
-// phase 1: every unit's Quantized tiles in groups of q_per — and each stream is split into
-// P equal contiguous ranges, one per CTA, so every CTA gets the same bytes of each kind
-// (the two kinds cost differently: HBM-bound vs. ALU-heavy).  A CTA streams its phase-0
-// range, then its phase-1 range.
-struct PlanView {
-  // per phase f: cta_lo [P + 1] first item of each CTA's range (cta_lo(f)[P] = items);
-  // cta_u0 [P] unit (index in the call) of item cta_lo(f)[c]; item_first [U + 1] first item
-  // of each unit; cta_first / cta_last [U] CTAs covering the unit's phase-f items
-  // (cta_last = cta_first - 1 when it has none).  Then part_base [U + 1]: first partial
-  // slot of each unit (C slots per covering CTA, phase 0 first).
-  const int32_t* base;
-  int U, P, ps;  // ps: ints per phase
-  __host__ __device__ PlanView(const int32_t* p, int U_, int P_) : base(p), U(U_), P(P_), ps(2 * P_ + 3 * U_ + 2) {}
-  __host__ __device__ const int32_t* cta_lo(int f) const { return base + f * ps; }
-  __host__ __device__ const int32_t* cta_u0(int f) const { return base + f * ps + P + 1; }
-  __host__ __device__ const int32_t* item_first(int f) const { return base + f * ps + 2 * P + 1; }
-  __host__ __device__ const int32_t* cta_first(int f) const { return base + f * ps + 2 * P + U + 2; }
-  __host__ __device__ const int32_t* cta_last(int f) const { return base + f * ps + 2 * P + 2 * U + 2; }
-  __host__ __device__ const int32_t* part_base() const { return base + 2 * ps; }
-};
-__host__ __device__ inline int plan_ints(int U, int P) { return 2 * (2 * P + 1 + 3 * U + 1) + U + 1; }
+// Work plan of the persistent decode kernel, passed by value as a kernel
+// parameter (no host-to-device copy in the stream).  The step's items form two streams —
+// phase 0: every unit's Original tiles (16 KB each); phase 1: every unit's Quantized tiles
+// in groups of q_per — and each stream is cut into P equal contiguous ranges, one per CTA,
+// so every CTA gets the same bytes of each kind (the kinds cost differently: HBM-bound vs.
+// ALU-heavy).  A CTA streams its phase-0 range, then its phase-1 range; the kernel walks
+// unit boundaries itself from the descriptors.
 constexpr int kPersistConsumers = 4;
-// a unit's partials are listed in shared memory by its combine: the host plan keeps every
-// unit within kMaxUnitParts / kPersistConsumers CTAs
+constexpr int kPlanMaxCtas = 320;  // 2 CTAs/SM x <= 160 SMs
+// partial slots one combine merges (C per covering CTA and phase)
 constexpr int kMaxUnitParts = 512;
+struct PersistPlan {
+  int P;
+  // per phase, per CTA: x = unit (index in the call) of its first item, y = that item's
+  // index within the unit, z = items in the range, w = first partial slot of the range
+  // (C slots per unit from x to ue; a unit in both of a CTA's ranges uses its phase-0 slots)
+  int4 cta[2][kPlanMaxCtas];
+  int ue[2][kPlanMaxCtas];  // unit of the range's last item
+};
 struct PlanArgs {
-  const int32_t* plan = nullptr;  // device PlanView ints, or nullptr: split-K kernels
-  int U = 0, P = 0;
+  const PersistPlan* plan = nullptr;  // host plan, or nullptr: split-K kernels
   float* pparts = nullptr;
+  int4* pcta = nullptr;
+  int32_t* pcover = nullptr;
 };
 
 // Decode attention (D1, D3, D7) for units [layer0, layer0+n) of all sequences.
