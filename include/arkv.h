@@ -187,6 +187,17 @@ arkv_status arkv_schedule(const arkv_config* cfg, int32_t prompt_len, double rho
    the tailor's packing pass inverts the forward map.  ARKV_ERR_DEVICE on a violation. */
 arkv_status arkv_layout_check(const arkv_config* cfg, int64_t* n_checked);
 
+/* Host only.  Builds the persistent decode kernel's work plan (decode_kernel = 3;
+   DESIGN.md §6) for n_units units with the given Original / Quantized row counts and at
+   most max_ctas CTAs, then replays one step on the host — the producer's unit-merged item
+   order, each consumer warp's partial slot, the coverage table and the combine's slot
+   enumeration — checking that every item is streamed exactly once, no two partials share
+   a slot, and each unit's combine merges exactly its own partials.  *ctas_used = the grid
+   the plan chose.  ARKV_ERR_DEVICE on a violated invariant, ARKV_ERR_INVALID_ARG on
+   counts outside the cache's capacity. */
+arkv_status arkv_persist_plan_check(const arkv_config* cfg, const int32_t* n_o, const int32_t* n_q,
+                                    int32_t n_units, int32_t max_ctas, int32_t* ctas_used);
+
 /* Host only.  Statistics -> OQ score (Eq. 6 with the R6 clamps applied to the raw
    moments). */
 arkv_status arkv_oq_score(const arkv_config* cfg, double entropy, double m2, double m4, double* stats3,

@@ -47,7 +47,7 @@ EXPORTED = [
     "arkv_prefill_stats", "arkv_decode_step", "arkv_unit_counts", "arkv_export_unit",
     "arkv_check", "arkv_schedule", "arkv_oq_score", "arkv_launch_count", "arkv_version",
     "arkv_status_string", "arkv_cache_info", "arkv_prefill_begin", "arkv_prefill_finish",
-    "arkv_profile", "arkv_profile_read", "arkv_layout_check",
+    "arkv_profile", "arkv_profile_read", "arkv_layout_check", "arkv_persist_plan_check",
 ]
 
 _lib = None
@@ -73,6 +73,7 @@ def lib() -> ctypes.CDLL:
         L.arkv_schedule.argtypes = [P(ArkvConfig), i32, dbl, i32, P(i32), i32, P(i32)]
         L.arkv_oq_score.argtypes = [P(ArkvConfig), dbl, dbl, dbl, P(dbl), P(dbl)]
         L.arkv_layout_check.argtypes = [P(ArkvConfig), P(ctypes.c_int64)]
+        L.arkv_persist_plan_check.argtypes = [P(ArkvConfig), P(i32), P(i32), i32, i32, P(i32)]
         L.arkv_cache_info.argtypes = [vp, i32]
         L.arkv_cache_info.restype = ctypes.c_int32
         L.arkv_prefill_begin.argtypes = [vp, vp, vp, i32, vp, vp]
@@ -137,6 +138,18 @@ def arkv_layout_check(cfg: ArkvConfig) -> int:
     n = ctypes.c_int64()
     _ok(lib().arkv_layout_check(ctypes.byref(cfg), ctypes.byref(n)), "arkv_layout_check")
     return n.value
+
+
+def arkv_persist_plan_check(cfg: ArkvConfig, n_o, n_q, max_ctas: int) -> int:
+    """Builds the persistent kernel's plan for these per-unit counts and replays it on the
+    host (include/arkv.h); raises ArkvError on a violated invariant.  Returns the grid size."""
+    n = len(n_o)
+    a = (ctypes.c_int32 * n)(*[int(x) for x in n_o])
+    b = (ctypes.c_int32 * n)(*[int(x) for x in n_q])
+    used = ctypes.c_int32()
+    _ok(lib().arkv_persist_plan_check(ctypes.byref(cfg), a, b, n, max_ctas, ctypes.byref(used)),
+        "arkv_persist_plan_check")
+    return used.value
 
 
 def arkv_oq_score(cfg: ArkvConfig, entropy: float, m2: float, m4: float):

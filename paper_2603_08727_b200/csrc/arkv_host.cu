@@ -642,25 +642,27 @@ arkv_status arkv_prefill_stats(arkv_cache* c, const void* q_win, const void* k, 
 // Quantized tiles in groups of q_per.  Each phase's item stream is cut into P equal ranges;
 // a range's partial slots are C per unit it spans.  P shrinks until no unit needs more
 // than kMaxUnitParts slots.
-void build_plan(const arkv_cache* c, int layer0, int n_layers, int P, PersistPlan* plan) {
-  const Geom& g = c->g;
-  const int U = g.batch * n_layers * g.Hkv;
+int persist_items(const Geom& g, int n_o, int n_q, int f) {
   const int q_per = (32 * 4 * g.d) / g.tile_q;  // Quantized tiles per 16 KB ring stage
+  const int tiles_q = (n_q + kTile - 1) / kTile;
+  return f == 0 ? (n_o + kTile - 1) / kTile : (tiles_q + q_per - 1) / q_per;
+}
+
+// Plan for U units with the given per-unit counts (units in call order).
+void build_plan_counts(const Geom& g, int U, const int* n_o, const int* n_q, int P, PersistPlan* plan) {
   std::vector<int64_t> first[2];
   for (int f = 0; f < 2; ++f) first[f].assign(U + 1, 0);
-  for (int ul = 0; ul < U; ++ul) {
-    const int b = ul / (n_layers * g.Hkv), li = (ul / g.Hkv) % n_layers;
-    const int bl = b * g.L + layer0 + li;
-    const int tiles_o = (c->n_o[bl] + kTile - 1) / kTile, tiles_q = (c->n_q[bl] + kTile - 1) / kTile;
-    first[0][ul + 1] = first[0][ul] + tiles_o;
-    first[1][ul + 1] = first[1][ul] + (tiles_q + q_per - 1) / q_per;
-  }
+  for (int ul = 0; ul < U; ++ul)
+    for (int f = 0; f < 2; ++f) first[f][ul + 1] = first[f][ul] + persist_items(g, n_o[ul], n_q[ul], f);
   const int64_t N = std::max(first[0][U], first[1][U]);
   P = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(P, kPlanMaxCtas), N));
-  std::vector<int> cover(U);
+  std::vector<int> cf[2], cl[2];
   const int64_t cap = (int64_t)2 * (kPlanMaxCtas + g.n_units) * kPersistConsumers;  // compute_sizes
   for (;;) {
-    std::fill(cover.begin(), cover.end(), 0);
+    for (int f = 0; f < 2; ++f) {
+      cf[f].assign(U, -1);
+      cl[f].assign(U, -1);
+    }
     int64_t slots = 0;
     for (int f = 0; f < 2; ++f) {
       const int64_t Nf = first[f][U];
@@ -676,19 +678,160 @@ void build_plan(const arkv_cache* c, int layer0, int n_layers, int P, PersistPla
           r.x = ul;
           r.y = (int)(i0 - first[f][ul]);
           slots += (int64_t)(ue - ul + 1) * kPersistConsumers;
+          // the combine enumerates every CTA between a unit's first and last covering one
           for (int u = ul; u <= ue; ++u)
-            if (first[f][u + 1] > first[f][u]) ++cover[u];
+            if (first[f][u + 1] > first[f][u]) {
+              if (cf[f][u] < 0) cf[f][u] = k;
+              cl[f][u] = k;
+            }
         }
         plan->cta[f][k] = r;
         plan->ue[f][k] = ue;
       }
     }
     int span_max = 0;
-    for (int u = 0; u < U; ++u) span_max = std::max(span_max, cover[u]);
+    for (int u = 0; u < U; ++u) {
+      int n = 0;
+      for (int f = 0; f < 2; ++f)
+        if (cf[f][u] >= 0) n += cl[f][u] - cf[f][u] + 1;
+      span_max = std::max(span_max, n);
+    }
     if ((span_max * kPersistConsumers <= kMaxUnitParts && slots <= cap) || P == 1) break;
     P = std::max(1, P * 3 / 4);  // too few units for this many CTAs: fewer, longer ranges
   }
   plan->P = P;
+}
+
+void build_plan(const arkv_cache* c, int layer0, int n_layers, int P, PersistPlan* plan) {
+  const Geom& g = c->g;
+  const int U = g.batch * n_layers * g.Hkv;
+  std::vector<int> no(U), nq(U);
+  for (int ul = 0; ul < U; ++ul) {
+    const int b = ul / (n_layers * g.Hkv), li = (ul / g.Hkv) % n_layers;
+    const int bl = b * g.L + layer0 + li;
+    no[ul] = c->n_o[bl];
+    nq[ul] = c->n_q[bl];
+  }
+  build_plan_counts(g, U, no.data(), nq.data(), P, plan);
+}
+
+// Host replay of one persistent step under a plan (the producer's unit-merged order, the
+// consumer warps' partial slots, the coverage table and the combine's enumeration), checking
+// every invariant the kernels rely on.  Returns false on a violation.
+static int fail_line = 0;
+bool replay_plan(const Geom& g, int U, const int* n_o, const int* n_q, const PersistPlan& plan) {
+  constexpr int C = kPersistConsumers;
+  const int P = plan.P;
+  const int64_t cap = (int64_t)2 * (kPlanMaxCtas + g.n_units) * C;
+  auto items = [&](int u, int f) { return persist_items(g, n_o[u], n_q[u], f); };
+  std::vector<std::vector<int>> seen(2);
+  for (int f = 0; f < 2; ++f) {
+    int64_t n = 0;
+    for (int u = 0; u < U; ++u) n += items(u, f);
+    seen[f].assign((size_t)n, 0);
+  }
+  std::vector<int64_t> first[2];
+  for (int f = 0; f < 2; ++f) {
+    first[f].assign(U + 1, 0);
+    for (int u = 0; u < U; ++u) first[f][u + 1] = first[f][u] + items(u, f);
+  }
+  std::vector<int> cover(4 * U, -1);
+  std::vector<int> slot_unit((size_t)cap, -1);
+  for (int c = 0; c < P; ++c) {
+    int ul[2], k[2], rem[2];
+    for (int f = 0; f < 2; ++f) {
+      ul[f] = plan.cta[f][c].x;
+      k[f] = plan.cta[f][c].y;
+      rem[f] = plan.cta[f][c].z;
+    }
+    std::vector<int> seq;
+    const int n_work = rem[0] + rem[1];
+    for (int j = 0; j < n_work; ++j) {
+      const int f = (rem[0] > 0 && (rem[1] <= 0 || ul[0] <= ul[1])) ? 0 : 1;
+      if (ul[f] < 0 || ul[f] >= U || k[f] < 0 || k[f] >= items(ul[f], f)) { fail_line = __LINE__; return false; }
+      const int64_t gi = first[f][ul[f]] + k[f];
+      if (seen[f][(size_t)gi]++) { fail_line = __LINE__; return false; }  // processed twice
+      if (k[f] == 0) cover[(f * 2 + 0) * U + ul[f]] = c;
+      if (k[f] == items(ul[f], f) - 1) cover[(f * 2 + 1) * U + ul[f]] = c;
+      seq.push_back(ul[f]);
+      if (--rem[f] > 0) {
+        ++k[f];
+        while (k[f] >= items(ul[f], f)) {
+          k[f] -= items(ul[f], f);
+          if (++ul[f] >= U) { fail_line = __LINE__; return false; }
+        }
+      }
+    }
+    for (int w = 0; w < C; ++w) {
+      int cur = -1;
+      std::vector<int> done;
+      for (int j = w; j < n_work; j += C) {
+        if (seq[j] == cur) continue;
+        cur = seq[j];
+        for (int d : done)
+          if (d == cur) { fail_line = __LINE__; return false; }  // a warp must see each unit once
+        done.push_back(cur);
+        const int4 r0 = plan.cta[0][c];
+        const bool in0 = r0.z > 0 && cur >= r0.x && cur <= plan.ue[0][c];
+        const int4 r = in0 ? r0 : plan.cta[1][c];
+        const int64_t slot = r.w + (int64_t)(cur - r.x) * C + w;
+        if (slot < 0 || slot >= cap || slot_unit[(size_t)slot] != -1) { fail_line = __LINE__; return false; }
+        slot_unit[(size_t)slot] = cur;
+      }
+    }
+  }
+  for (int f = 0; f < 2; ++f)
+    for (int v : seen[f])
+      if (v != 1) { fail_line = __LINE__; return false; }  // every item exactly once
+  for (int u = 0; u < U; ++u) {
+    std::vector<int64_t> en;
+    for (int f = 0; f < 2; ++f) {
+      const int cf = cover[(f * 2 + 0) * U + u], cl = cover[(f * 2 + 1) * U + u];
+      if (cf < 0) continue;
+      for (int cc = cf; cc <= cl; ++cc) {
+        const int4 r = plan.cta[f][cc];
+        if (r.z <= 0) continue;
+        int4 pc = make_int4(r.x, r.w, plan.ue[f][cc], 0);
+        if (f == 1) {
+          const int4 q0 = plan.cta[0][cc];
+          if (q0.z > 0 && u >= q0.x && u <= plan.ue[0][cc]) {
+            pc = make_int4(q0.x, q0.w, plan.ue[0][cc], 0);
+            const int cf0 = cover[u], cl0 = cover[U + u];
+            if (cf0 >= 0 && cc >= cf0 && cc <= cl0) continue;
+          }
+        }
+        for (int w = 0; w < C; ++w) en.push_back(pc.y + (int64_t)(u - pc.x) * C + w);
+      }
+    }
+    const int nc = (cover[u] >= 0 ? (cover[U + u] - cover[u] + 1) * C : 0) +
+                   (cover[2 * U + u] >= 0 ? (cover[3 * U + u] - cover[2 * U + u] + 1) * C : 0);
+    if (nc > kMaxUnitParts) { fail_line = __LINE__; return false; }
+    std::sort(en.begin(), en.end());
+    if (std::adjacent_find(en.begin(), en.end()) != en.end()) { fail_line = __LINE__; return false; }  // merged twice
+    for (int64_t sl : en)
+      if (sl < 0 || sl >= cap || (slot_unit[(size_t)sl] != -1 && slot_unit[(size_t)sl] != u)) { fail_line = __LINE__; return false; }
+    for (int64_t sl = 0; sl < cap; ++sl)
+      if (slot_unit[(size_t)sl] == u && !std::binary_search(en.begin(), en.end(), sl)) { fail_line = __LINE__; return false; }  // lost
+  }
+  return true;
+}
+
+arkv_status arkv_persist_plan_check(const arkv_config* cfg, const int32_t* n_o, const int32_t* n_q, int32_t n_units,
+                                    int32_t max_ctas, int32_t* ctas_used) {
+  arkv_status st = validate(cfg);
+  if (st != ARKV_OK) return st;
+  if (!n_o || !n_q || n_units <= 0) return ARKV_ERR_INVALID_ARG;
+  Sizes s = compute_sizes(*cfg);
+  if (n_units > s.g.n_units) return ARKV_ERR_INVALID_ARG;
+  for (int u = 0; u < n_units; ++u)
+    if (n_o[u] < 0 || n_q[u] < 0 || n_o[u] > s.g.cap_o || n_q[u] > s.g.cap_q) return ARKV_ERR_INVALID_ARG;
+  PersistPlan* plan = new PersistPlan();
+  build_plan_counts(s.g, n_units, n_o, n_q, max_ctas, plan);
+  const bool ok = replay_plan(s.g, n_units, n_o, n_q, *plan);
+  if (!ok && std::getenv("ARKV_DEBUG_PLAN")) std::fprintf(stderr, "replay_plan: violation at arkv_host.cu:%d\n", fail_line);
+  if (ctas_used) *ctas_used = plan->P;
+  delete plan;
+  return ok ? ARKV_OK : ARKV_ERR_DEVICE;
 }
 
 arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, const void* q, const void* k,

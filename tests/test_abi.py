@@ -111,3 +111,39 @@ def test_tile_layouts_are_bijections(d, bits, g, layout):
                       max_positions=256)
     n = A.arkv_layout_check(c)
     assert n == 32 * d * 2 + 32 * d * 2 + 32 * 4 * (d // g)
+
+
+@settings(max_examples=300, deadline=None)
+@given(n_layers=st.integers(1, 6), batch=st.integers(1, 3), hkv=st.sampled_from([1, 2, 8]),
+       max_ctas=st.sampled_from([1, 3, 40, 296, 320]), data=st.data())
+def test_persist_plan_replay(n_layers, batch, hkv, max_ctas, data):
+    """The persistent decode kernel's plan (host C++), replayed on the host: every item
+    streamed once, partial slots disjoint, each unit's combine merges exactly its own
+    partials — for arbitrary per-unit O/Q counts, including empty units and more CTAs
+    than items."""
+    B = 2048
+    c = A.make_config(n_layers, 4 * hkv, hkv, 128, batch=batch, window=32, budget_tokens=B,
+                      max_positions=4 * B, layout=2)
+    U = batch * n_layers * hkv
+    counts = st.tuples(st.integers(0, B + 1), st.integers(0, 3 * B))
+    pairs = data.draw(st.lists(counts, min_size=U, max_size=U))
+    n_o = [p[0] for p in pairs]
+    n_q = [p[1] for p in pairs]
+    if sum(n_o) + sum(n_q) == 0:
+        n_o[0] = 1
+    used = A.arkv_persist_plan_check(c, n_o, n_q, max_ctas)
+    assert 1 <= used <= max_ctas
+
+
+def test_persist_plan_configs1_keeps_full_grid():
+    """configs[1]-like counts (per-layer rho): the plan keeps 2 CTAs per SM."""
+    c = A.make_config(32, 32, 8, 128, window=32, budget_tokens=8192, max_positions=40000, layout=2)
+    rng = np.random.default_rng(0)
+    n_o, n_q = [], []
+    for _ in range(32):
+        rho = rng.uniform(0.05, 0.95)
+        o = int(rho * 8160) + 32
+        q = int((8192 - o) * 512 / 144)
+        n_o += [o] * 8
+        n_q += [q] * 8
+    assert A.arkv_persist_plan_check(c, n_o, n_q, 296) == 296
