@@ -880,7 +880,11 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
       if (t >= c->trig[bl] - g.W && t < c->trig[bl])  // HH accumulation step (R19)
         acc_rows = std::max(acc_rows, c->n_o[bl] + 1 + c->n_q[bl]);
     }
-  if (!jobs.empty()) {
+  // ARKV_TIMING_SKIP (timing experiments only; results are wrong): bit 0 skips the tailor
+  // launches, bit 1 the HH accumulation, so a bench run isolates their share of a step
+  static const int skip = std::getenv("ARKV_TIMING_SKIP") ? std::atoi(std::getenv("ARKV_TIMING_SKIP")) : 0;
+  if (skip & 2) acc_rows = 0;
+  if (!jobs.empty() && !(skip & 1)) {
     arkv_status st = run_jobs(c, jobs, nullptr, nullptr, 0, s);
     if (st != ARKV_OK) return st;
   }

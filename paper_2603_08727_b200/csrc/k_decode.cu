@@ -366,8 +366,8 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
     a.interleave = e2 ? std::atoi(e2) : 0;        // measured: interleaving O/Q items is slower
     const char* e3 = std::getenv("ARKV_FUSE_COMBINE");
     a.fuse_combine = e3 ? std::atoi(e3) : 0;      // measured: the separate combine kernel is faster
-    const char* e4 = std::getenv("ARKV_PRODUCER");
-    a.producer_mode = e4 ? std::atoi(e4) : 0;  // measured: in-order refill beats polling
+    const char* e4 = std::getenv("ARKV_ITEM_ORDER");
+    a.item_order = e4 ? std::atoi(e4) : 0;
   }
   a.out = out;
   a.out_fp32 = out_fp32;

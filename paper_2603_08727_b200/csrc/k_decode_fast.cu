@@ -540,8 +540,10 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536)
   const int q_per = a.q_group > 0 ? min(a.q_group, kStageBytes / g.tile_q) : kStageBytes / g.tile_q;
   const int n_oi = o1 - o0, n_qi = (q1 - q0 + q_per - 1) / q_per;
   const int n_work = n_oi + n_qi;
+  const bool rev = a.item_order == 2 || (a.item_order == 1 && ((s + ul) & 1));
   auto item_of = [&](int i, bool& isq, int& first, int& ntiles) {
     int qb;
+    if (rev) i = i < n_qi ? n_oi + i : i - n_qi;  // Quantized groups first
     if (a.interleave) {
       qb = (int)(((int64_t)i * n_qi) / max(n_work, 1));
       isq = (int)(((int64_t)(i + 1) * n_qi) / max(n_work, 1)) > qb;

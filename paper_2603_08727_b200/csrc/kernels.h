@@ -58,7 +58,8 @@ struct DecodeArgs {
   int q_group;        // fast kernel: Quantized tiles per bulk copy (0 = as many as fit a stage)
   int interleave;     // fast kernel: interleave Original and Quantized work items
   int fuse_combine;   // fast kernel: the last split CTA of a unit merges the partials
-  int producer_mode;  // fast kernel: 0 refill stages in item order, 1 whichever frees first
+  int item_order;     // fast kernel: 0 Original tiles first; 1 Quantized groups first on odd
+                      // (split + unit) CTAs; 2 Quantized groups first everywhere
   void* out;
   int out_fp32;
   int32_t* err;
