@@ -881,7 +881,8 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
         acc_rows = std::max(acc_rows, c->n_o[bl] + 1 + c->n_q[bl]);
     }
   // ARKV_TIMING_SKIP (timing experiments only; results are wrong): bit 0 skips the tailor
-  // launches, bit 1 the HH accumulation, so a bench run isolates their share of a step
+  // launches, bit 1 the HH accumulation, bit 2 the split combine, so a bench run isolates
+  // their share of a step
   static const int skip = std::getenv("ARKV_TIMING_SKIP") ? std::atoi(std::getenv("ARKV_TIMING_SKIP")) : 0;
   if (skip & 2) acc_rows = 0;
   if (!jobs.empty() && !(skip & 1)) {

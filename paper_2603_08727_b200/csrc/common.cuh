@@ -14,7 +14,8 @@
 //           operand of QK^T, V transposed as the A operand of PV), so the fast
 //           decode kernel streams tiles with fully coalesced 128-bit loads and no
 //           shared-memory transposes.  Q tiles store 4-bit codes nibble-interleaved
-//           for the fp16 "magic number" unpack (one LOP3 per two codes).
+//           for the fp16 "magic number" unpack (one LOP3 per two codes); per-token
+//           scale/zero quads after the codes.
 #pragma once
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -147,7 +148,9 @@ __host__ __device__ inline void q_v_loc(const Geom& g, int j, int x, int* byte, 
 // which: 0 k_scale, 1 k_zero, 2 v_scale, 3 v_zero.
 __host__ __device__ inline int q_sc_off(const Geom& g, int j, int which, int grp) {
   if (g.layout != ARKV_LAYOUT_FRAG) return j * g.cost_q + 2 * (g.d * g.bits >> 3) + (which * g.ng + grp) * 4;
-  return 32 * g.d + ((which * g.ng + grp) * 32 + j) * 4;
+  // per row and group the four floats k_scale, k_zero, v_scale, v_zero are adjacent: one
+  // 16-byte shared-memory load each in the decode kernel (conflict-free: rows 16 B apart)
+  return 32 * g.d + ((j * g.ng + grp) * 4 + which) * 4;
 }
 
 // Inverse of q_k_loc / q_v_loc: the code held by slot s (s < 8/bits, at bit s*bits) of

@@ -150,6 +150,13 @@ __device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
   __half2 v = __floats2half2_rn(lo, hi);
   return *(uint32_t*)&v;
 }
+// 2^x on the SFU without exp2f's denormal-range fix-up (results below 2^-126 flush to 0:
+// such probabilities are negligible next to the running max's 1)
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 __device__ __forceinline__ float f16_round(float x) { return __half2float(__float2half_rn(x)); }
 __device__ __forceinline__ uint32_t word(const uint4& q, int i) { return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w; }
@@ -307,7 +314,7 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
       for (int e = 0; e < 4; ++e) lg[mt][e] = acc[e] * c2;
     }
   } else {
-    const float* sc = (const float*)(tb + 32 * D);  // [which][grp][32]
+    const float* sc = (const float*)(tb + 32 * D);  // [row][grp][k_scale, k_zero, v_scale, v_zero]
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       float acc[NG][4];
@@ -332,10 +339,9 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
         float l0 = 0.f, l1 = 0.f;
 #pragma unroll
         for (int gr = 0; gr < NG; ++gr) {
-          const float ks = sc[(0 * NG + gr) * 32 + j];
-          float kz = sc[(1 * NG + gr) * 32 + j];
-          const float vs = sc[(2 * NG + gr) * 32 + j];
-          float vz = sc[(3 * NG + gr) * 32 + j];
+          const float4 s4 = *(const float4*)(sc + (j * NG + gr) * 4);  // one LDS.128 per row and group
+          const float ks = s4.x, vs = s4.z;
+          float kz = s4.y, vz = s4.w;
           if (sym) {
             kz = -8.f * ks;
             vz = -8.f * vs;
@@ -384,7 +390,7 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const float mn = fmaxf(s.m_run[e], tmax[e]);
-    corr[e] = (mn == -INFINITY) ? 1.f : exp2f(s.m_run[e] - mn);
+    corr[e] = (mn == -INFINITY) ? 1.f : ex2_ftz(s.m_run[e] - mn);
     s.m_run[e] = mn;
     s.l_run[e] *= corr[e];
 #pragma unroll
@@ -409,7 +415,7 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float mm = s.m_run[e & 1];
-      p[mt][e] = (lg[mt][e] == -INFINITY) ? 0.f : exp2f(lg[mt][e] - mm);
+      p[mt][e] = (mm == -INFINITY) ? 0.f : ex2_ftz(lg[mt][e] - mm);  // ex2(-inf) = 0 for masked rows
       s.l_run[e & 1] += p[mt][e];
     }
 
@@ -454,7 +460,7 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
       for (int gr = 0; gr < NG; ++gr) {
         float vsc[2];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) vsc[hh] = sc[(2 * NG + gr) * 32 + kc * 16 + gq + 8 * hh];
+        for (int hh = 0; hh < 2; ++hh) vsc[hh] = sc[((kc * 16 + gq + 8 * hh) * NG + gr) * 4 + 2];
         float pv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) pv[e] = p[kc][e] * vsc[e >> 1] * ((e >> 1) ? 0.0625f : 1.f);
@@ -1198,6 +1204,9 @@ int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
   }
   if (r < 0) return -1;
   if (a.fuse_combine) return 1;  // the last split CTA of each unit merged the partials
+  // ARKV_TIMING_SKIP bit 2 (timing experiments only, results wrong): no combine
+  static const int skip = std::getenv("ARKV_TIMING_SKIP") ? std::atoi(std::getenv("ARKV_TIMING_SKIP")) : 0;
+  if (skip & 4) return 1;
   launch_decode_combine(a, n_units_call, s);
   return 2;
 }
