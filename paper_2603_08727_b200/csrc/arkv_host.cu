@@ -746,8 +746,9 @@ bool replay_plan(const Geom& g, int U, const int* n_o, const int* n_q, const Per
     }
     std::vector<int> seq;
     const int n_work = rem[0] + rem[1];
+    const bool q_first = (c & 1) != 0;  // default item order (decode_persist_kernel)
     for (int j = 0; j < n_work; ++j) {
-      const int f = (rem[0] > 0 && (rem[1] <= 0 || ul[0] <= ul[1])) ? 0 : 1;
+      const int f = (rem[0] > 0 && (rem[1] <= 0 || (q_first ? ul[0] < ul[1] : ul[0] <= ul[1]))) ? 0 : 1;
       if (ul[f] < 0 || ul[f] >= U || k[f] < 0 || k[f] >= items(ul[f], f)) { fail_line = __LINE__; return false; }
       const int64_t gi = first[f][ul[f]] + k[f];
       if (seen[f][(size_t)gi]++) { fail_line = __LINE__; return false; }  // processed twice

@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(128) decode_split_generic(DecodeArgs a) {
 
 // Combine: merge split partials, write the output, HH accumulation, advance the unit.
 template <int G>
-__global__ void __launch_bounds__(256) decode_combine(DecodeArgs a) {
+__global__ void __launch_bounds__(1024) decode_combine(DecodeArgs a) {
   griddep_wait();
   griddep_launch_dependents();
   int b, li, kvh, u;
@@ -302,6 +302,9 @@ int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
                        const PersistPlan* plan);
 void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s);
 
+// one combine thread per (head, dim) up to 1024 (measured: latency-bound otherwise)
+static int combine_threads(const Geom& g) { return std::min(1024, std::max(128, (g.G * g.d + 31) / 32 * 32)); }
+
 template <int G>
 static void launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
   dim3 grid(a.n_splits, n_units_call);
@@ -322,15 +325,15 @@ static void launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cuda
       break;
   }
   if (ev1) cudaEventRecord(ev1, s);
-  launch_pdl(decode_combine<G>, dim3(n_units_call), dim3(256), 0, s, a);
+  launch_pdl(decode_combine<G>, dim3(n_units_call), dim3(combine_threads(a.g)), 0, s, a);
 }
 
 void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s) {
   switch (a.g.G) {
-    case 1: launch_pdl(decode_combine<1>, dim3(n_units_call), dim3(256), 0, s, a); break;
-    case 2: launch_pdl(decode_combine<2>, dim3(n_units_call), dim3(256), 0, s, a); break;
-    case 4: launch_pdl(decode_combine<4>, dim3(n_units_call), dim3(256), 0, s, a); break;
-    case 8: launch_pdl(decode_combine<8>, dim3(n_units_call), dim3(256), 0, s, a); break;
+    case 1: launch_pdl(decode_combine<1>, dim3(n_units_call), dim3(combine_threads(a.g)), 0, s, a); break;
+    case 2: launch_pdl(decode_combine<2>, dim3(n_units_call), dim3(combine_threads(a.g)), 0, s, a); break;
+    case 4: launch_pdl(decode_combine<4>, dim3(n_units_call), dim3(combine_threads(a.g)), 0, s, a); break;
+    case 8: launch_pdl(decode_combine<8>, dim3(n_units_call), dim3(combine_threads(a.g)), 0, s, a); break;
     default: break;
   }
 }

@@ -814,13 +814,16 @@ __device__ __forceinline__ const uint16_t* punit_q(const DecodeArgs& a, int ul) 
   const int li = rem / g.Hkv, kvh = rem % g.Hkv;
   return a.q + ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * g.G) * D;
 }
-__device__ __forceinline__ void punit_load(const DecodeArgs& a, int ul, int f, int q_per, PUnit& p) {
+__device__ __forceinline__ int punit_global(const DecodeArgs& a, int ul) {
   const Geom& g = a.g;
   const int b = ul / (a.n_layers * g.Hkv);
   const int rem = ul % (a.n_layers * g.Hkv);
-  const int li = rem / g.Hkv, kvh = rem % g.Hkv;
-  p.u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
-  const UnitDesc dsc = a.desc[p.u];
+  return (b * g.L + a.layer0 + rem / g.Hkv) * g.Hkv + rem % g.Hkv;
+}
+__device__ __forceinline__ void punit_fill(const DecodeArgs& a, const UnitDesc& dsc, int u, int f, int q_per,
+                                           PUnit& p) {
+  const Geom& g = a.g;
+  p.u = u;
   p.slot = dsc.slot;
   p.n_o = dsc.n_o;
   p.n_q = dsc.n_q;
@@ -829,22 +832,34 @@ __device__ __forceinline__ void punit_load(const DecodeArgs& a, int ul, int f, i
   p.accm = (dsc.t_next >= dsc.trig - g.W) && (dsc.t_next < dsc.trig);
 }
 // Position in one phase range of a CTA: item k of unit ul.  Walks forward only (units
-// with no items of the phase are stepped over).
+// with no items of the phase are stepped over); the next unit's descriptor is prefetched
+// so a unit change does not stall the producer on a dependent load.
 struct Walker {
-  int ul, k, rem;
+  int ul, k, rem, U;
   PUnit p;
-  __device__ __forceinline__ void init(const DecodeArgs& a, const int4& r, int f, int q_per) {
+  UnitDesc nxt;
+  __device__ __forceinline__ void prefetch(const DecodeArgs& a) {
+    if (ul + 1 < U) nxt = a.desc[punit_global(a, ul + 1)];
+  }
+  __device__ __forceinline__ void init(const DecodeArgs& a, const int4& r, int f, int q_per, int n_units) {
     ul = r.x;
     k = r.y;
     rem = r.z;
-    if (rem > 0) punit_load(a, ul, f, q_per, p);
+    U = n_units;
+    if (rem > 0) {
+      const int u = punit_global(a, ul);
+      punit_fill(a, a.desc[u], u, f, q_per, p);
+      prefetch(a);
+    }
   }
   __device__ __forceinline__ void next(const DecodeArgs& a, int f, int q_per) {
     if (--rem <= 0) return;
     ++k;
     while (k >= p.items) {
       k -= p.items;
-      punit_load(a, ++ul, f, q_per, p);
+      ++ul;
+      punit_fill(a, nxt, punit_global(a, ul), f, q_per, p);
+      prefetch(a);
     }
   }
 };
@@ -896,8 +911,8 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
     // its Quantized groups) so each consumer warp accumulates a unit across both kinds ============
     if (lane == 0) {
       Walker w0, w1;
-      w0.init(a, plan.cta[0][c], 0, q_per);
-      w1.init(a, plan.cta[1][c], 1, q_per);
+      w0.init(a, plan.cta[0][c], 0, q_per, n_units_call);
+      w1.init(a, plan.cta[1][c], 1, q_per, n_units_call);
       auto issue = [&](Walker& w, int f, int j) {
         const PUnit& p = w.p;
         // the CTAs holding a unit's first and last item of the phase, for the combine
@@ -921,8 +936,11 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
         mbar_expect_tx(&sm.full[st], bytes);  // release: orders the info writes above
         bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
       };
+      // per unit: Original tiles first on even CTAs, Quantized groups first on odd ones, so
+      // co-resident CTAs tend to overlap HBM-bound and ALU-heavy work
+      const bool q_first = (c & 1) && a.item_order != 0;
       for (int j = 0; j < n_work; ++j) {
-        const bool take0 = w0.rem > 0 && (w1.rem <= 0 || w0.ul <= w1.ul);
+        const bool take0 = w0.rem > 0 && (w1.rem <= 0 || (q_first ? w0.ul < w1.ul : w0.ul <= w1.ul));
         if (take0) {
           issue(w0, 0, j);
           w0.next(a, 0, q_per);
@@ -1012,11 +1030,11 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
   if (cur >= 0) flush();
 }
 
-// One CTA (D threads) per unit: append the step's token (D1), its logits (and HH logit
-// row), merge the unit's warp partials with it, write the output and the merged row
-// statistics, advance the descriptor.
+// One CTA (G x D threads: one per head and dim) per unit: append the step's token (D1),
+// its logits (and HH logit row), merge the unit's warp partials with it, write the output
+// and the merged row statistics, advance the descriptor.
 template <int G>
-__global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
+__global__ void __launch_bounds__(G * D) decode_persist_combine(DecodeArgs a) {
   griddep_wait();
   griddep_launch_dependents();
   constexpr int C = kPersistConsumers;
@@ -1027,7 +1045,8 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
   const int li = rem / g.Hkv, kvh = rem % g.Hkv;
   const int u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
   const UnitDesc dsc = a.desc[u];
-  const int n_o = dsc.n_o, x = threadIdx.x, warp = x >> 5, lane = x & 31;
+  const int n_o = dsc.n_o, tid = threadIdx.x, h = tid / D, x = tid % D, lane = tid & 31;
+  const bool lead = x < 32;  // the first warp of head h's group
   const int64_t qkv = (int64_t)(b * a.n_layers + li);
   const uint16_t* qp = a.q + (qkv * g.Hq + kvh * G) * D;
   const uint16_t* kn = a.k + (qkv * g.Hkv + kvh) * D;
@@ -1039,27 +1058,30 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
   __shared__ int s_slot[kMaxUnitParts];
   __shared__ int s_cov[4];
   // ---- the CTAs covering the unit (first, last per phase); cleared for the next step ----
-  if (x < 4) s_cov[x] = a.pcover[(x >> 1) * 2 * n_units_call + (x & 1) * n_units_call + ul];
+  if (tid < 4) s_cov[tid] = a.pcover[(tid >> 1) * 2 * n_units_call + (tid & 1) * n_units_call + ul];
   // ---- append the token to the Original stack (row n_o) ----
-  const int tiles_o = (n_o + 1 + kTile - 1) / kTile, tiles_q = (dsc.n_q + kTile - 1) / kTile;
-  const bool fits = (n_o + 1 <= g.cap_o) && ((int64_t)tiles_o * g.tile_o + (int64_t)tiles_q * g.tile_q <= g.slot_bytes);
-  uint8_t* slot = a.slots + (int64_t)dsc.slot * g.slot_bytes;
-  const uint16_t kx = kn[x], vx = vn[x];
-  if (fits) {
-    uint8_t* tb = o_tile_ptr(slot, g, n_o / kTile);
-    *(uint16_t*)(tb + o_k_off(g, n_o % kTile, x)) = kx;
-    *(uint16_t*)(tb + o_v_off(g, n_o % kTile, x)) = vx;
-    if (x == 0) {
-      const SlotMeta meta = slot_meta(a.meta, g, dsc.slot);
-      meta.pos_o[n_o] = dsc.t_next;
-      meta.acc_o[n_o] = make_float2(0.f, 0.f);
+  const uint16_t vx = vn[x];
+  if (h == 0) {
+    const int tiles_o = (n_o + 1 + kTile - 1) / kTile, tiles_q = (dsc.n_q + kTile - 1) / kTile;
+    const bool fits =
+        (n_o + 1 <= g.cap_o) && ((int64_t)tiles_o * g.tile_o + (int64_t)tiles_q * g.tile_q <= g.slot_bytes);
+    uint8_t* slot = a.slots + (int64_t)dsc.slot * g.slot_bytes;
+    if (fits) {
+      uint8_t* tb = o_tile_ptr(slot, g, n_o / kTile);
+      *(uint16_t*)(tb + o_k_off(g, n_o % kTile, x)) = kn[x];
+      *(uint16_t*)(tb + o_v_off(g, n_o % kTile, x)) = vx;
+      if (x == 0) {
+        const SlotMeta meta = slot_meta(a.meta, g, dsc.slot);
+        meta.pos_o[n_o] = dsc.t_next;
+        meta.acc_o[n_o] = make_float2(0.f, 0.f);
+      }
+    } else if (x == 0) {
+      atomicOr(a.err, kErrCapacity);
     }
-  } else if (x == 0) {
-    atomicOr(a.err, kErrCapacity);
   }
-  // ---- its logits (log2 domain): warp w reduces heads w, w + 4 ----
+  // ---- its logit for head h (log2 domain) ----
   const float c2 = g.sm_scale * kLog2e;
-  for (int h = warp; h < G; h += D / 32) {
+  if (lead) {
     float acc = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc = fmaf(bf16_to_f(qp[h * D + lane * 4 + i]), bf16_to_f(kn[lane * 4 + i]), acc);
@@ -1071,14 +1093,14 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
     }
   }
   __syncthreads();
-  if (x < 4) a.pcover[(x >> 1) * 2 * n_units_call + (x & 1) * n_units_call + ul] = -1;
+  if (tid < 4) a.pcover[(tid >> 1) * 2 * n_units_call + (tid & 1) * n_units_call + ul] = -1;
   // ---- candidate partial slots: C per covering CTA and phase.  A slot whose warp processed
   // none of the unit's items holds l = 0 (slots start zeroed and every combine clears the
   // l of the slots it merged) ----
   const int nc0 = s_cov[0] >= 0 ? (s_cov[1] - s_cov[0] + 1) * C : 0;
   const int nc1 = s_cov[2] >= 0 ? (s_cov[3] - s_cov[2] + 1) * C : 0;
   const int ncand = min(nc0 + nc1, kMaxUnitParts);
-  for (int k = x; k < ncand; k += D) {
+  for (int k = tid; k < ncand; k += G * D) {
     const int f = k < nc0 ? 0 : 1, kk = f == 0 ? k : k - nc0;
     const int cc = s_cov[2 * f] + kk / C;
     int4 pc = a.pcta[f * kPlanMaxCtas + cc];
@@ -1097,8 +1119,8 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
   }
   __syncthreads();
   const float* pp = a.pparts;
-  // merged max and sum per head: warp w reduces heads w, w + 4
-  for (int h = warp; h < G; h += D / 32) {
+  // merged max and sum of head h (its lead warp)
+  if (lead) {
     float M = s_new[h];
     for (int k = lane; k < ncand; k += 32) {
       if (s_slot[k] < 0) continue;
@@ -1125,25 +1147,22 @@ __global__ void __launch_bounds__(D) decode_persist_combine(DecodeArgs a) {
     }
   }
   __syncthreads();
-  const int64_t obase = (qkv * g.Hq + kvh * G) * D;
-  const float vnew = bf16_to_f(vx);
-#pragma unroll
-  for (int h = 0; h < G; ++h) {
-    float O = exp2f(s_new[h] - sM[h]) * vnew;
-    for (int k = 0; k < ncand; ++k) {
-      const float w = s_w[k][h];
-      if (w != 0.f) O += __ldcg(pp + ((int64_t)s_slot[k] * G + h) * (D + 2) + 2 + x) * w;
-    }
-    O *= sIL[h];
-    if (a.out_fp32)
-      ((float*)a.out)[obase + h * D + x] = O;
-    else
-      ((uint16_t*)a.out)[obase + h * D + x] = f_to_bf16_rne(O);
+  float O = exp2f(s_new[h] - sM[h]) * bf16_to_f(vx);
+#pragma unroll 4
+  for (int k = 0; k < ncand; ++k) {
+    const float w = s_w[k][h];
+    if (w != 0.f) O += __ldcg(pp + ((int64_t)s_slot[k] * G + h) * (D + 2) + 2 + x) * w;
   }
+  O *= sIL[h];
+  const int64_t obase = (qkv * g.Hq + kvh * G) * D;
+  if (a.out_fp32)
+    ((float*)a.out)[obase + h * D + x] = O;
+  else
+    ((uint16_t*)a.out)[obase + h * D + x] = f_to_bf16_rne(O);
   // clear the merged slots' l for the next step's plan
-  for (int k = x; k < ncand * G; k += D)
+  for (int k = tid; k < ncand * G; k += G * D)
     if (s_slot[k / G] >= 0) a.pparts[((int64_t)s_slot[k / G] * G + k % G) * (D + 2) + 1] = 0.f;
-  if (x == 0) {
+  if (tid == 0) {
     UnitDesc nd = dsc;
     nd.n_o = n_o + 1;
     nd.t_next = dsc.t_next + 1;
@@ -1160,7 +1179,7 @@ static void launch_persist(const DecodeArgs& a, const PersistPlan& plan, int n_u
   if (ev0) cudaEventRecord(ev0, s);
   launch_pdl(kern, dim3(plan.P), dim3((kPersistConsumers + 1) * 32), (size_t)smem, s, a, plan);
   if (ev1) cudaEventRecord(ev1, s);
-  launch_pdl(decode_persist_combine<G>, dim3(n_units_call), dim3(D), 0, s, a);
+  launch_pdl(decode_persist_combine<G>, dim3(n_units_call), dim3(G * D), 0, s, a);
 }
 template <int G>
 static int launch_persist_g(const DecodeArgs& a, const PersistPlan& plan, int n_units_call, cudaStream_t s,
