@@ -304,8 +304,8 @@ def run_arkv(args, wl):
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp))
-            if tj.get("workload") == args.workload and tj.get("kernel_impl") == cache_kernel(cache):
-                traffic = tj.get("dram_bytes_per_launch")
+            if args.mode == "arkv":
+                traffic = tj.get(args.workload, {}).get(cache_kernel(cache), {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     budget_tokens = B * L * Hkv * budget

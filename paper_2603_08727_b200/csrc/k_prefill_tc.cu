@@ -11,7 +11,8 @@
 // 16-element K step issued by a single thread, accumulators double-buffered in TMEM
 // (2 x 128 fp32 columns) so the epilogue of tile i overlaps the MMA of tile i + 1,
 // completion signalled by tcgen05.commit on an mbarrier.  K tiles stream through a
-// 3-deep cp.async ring.  8 warps: warps w and w + 4 read the same 32 TMEM lanes, each
+// 2-deep cp.async ring (the next tile loads while the epilogue of the previous one runs),
+// so two CTAs fit an SM.  8 warps: warps w and w + 4 read the same 32 TMEM lanes, each
 // half of the 128 columns.
 #include "kernels.h"
 
@@ -24,18 +25,24 @@ constexpr int NK = 128;                // keys per tile
 constexpr int kChunk = 2048;           // keys per CTA (same partial layout as k_prefill.cu)
 constexpr int kSub = 128 * 128;        // one [128 rows x 64 bf16] SW128 sub-tile (16 KB)
 constexpr int kTileB = 2 * kSub;       // [128 x 128] bf16 = 32 KB
-constexpr int kBufs = 3;
+constexpr int kBufs = 2;  // 2 CTAs per SM (smem ~101 KB each; TMEM 2 x 256 columns)
 constexpr int kThreads = 256;
 
 struct __align__(8) Ctl {
   uint64_t mbar[2];
   uint32_t tmem;
-  float rowm[R], rowil[R];
+  float rowc[R];  // pass 2: row max + log2(row sum) of pass 1
   float red[2][R][2];  // combine of the two column halves
 };
 constexpr int kSmem = 1024 /*align slack*/ + kTileB * (1 + kBufs) + (int)sizeof(Ctl);
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// 2^x on the SFU without exp2f's denormal fix-up (values below 2^-126 flush to 0)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool pred) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(pred ? 16 : 0));
@@ -87,7 +94,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 
 template <bool PASS2>
-__global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(Geom g, const uint16_t* __restrict__ q_win,
+__global__ void __launch_bounds__(kThreads, 2) prefill_tc_kernel(Geom g, const uint16_t* __restrict__ q_win,
                                                                  const uint16_t* __restrict__ kmat, int P,
                                                                  float2* __restrict__ partials, int n_chunks1,
                                                                  float2* __restrict__ acc_pf) {
@@ -132,7 +139,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(Geom g, const u
     }
   };
   load_k(0);
-  asm volatile("cp.async.commit_group;\n");
   if (n_tiles > 1) load_k(1);
   asm volatile("cp.async.commit_group;\n");
   // row statistics of pass 1 (pass 2 only)
@@ -146,8 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(Geom g, const u
         const float2 v = pr[(int64_t)c * R];
         if (v.y > 0.f) L += v.y * exp2f(v.x - M);
       }
-      ctl.rowm[r] = M;
-      ctl.rowil[r] = 1.0f / L;
+      ctl.rowc[r] = M + log2f(L);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -162,6 +167,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(Geom g, const u
   auto epilogue = [&](int t) {
     const int acc = t & 1;
     mbar_wait(&ctl.mbar[acc], (t >> 1) & 1);
+    // MMA t is complete: its K buffer takes tile t + 2, loading behind this epilogue
+    if (t + 2 < n_tiles) load_k(t + 2);
+    asm volatile("cp.async.commit_group;\n");
     __syncwarp();  // tcgen05.ld is .aligned: reconverge after the spin-wait
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 128 + half * 64);
@@ -174,18 +182,27 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(Geom g, const u
         float v[32];
         tmem_ld32(taddr + cc * 32, v);
         float mx = -INFINITY;
+        const int key0 = kbase + half * 64 + cc * 32;
+        if (key0 + 31 < c1 && key0 + 31 <= P - g.W) {  // no key masked (all but the last tiles)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int key = kbase + half * 64 + cc * 32 + i;
-          v[i] = (key < c1 && key <= qp) ? v[i] * sl2 : -INFINITY;
-          mx = fmaxf(mx, v[i]);
+          for (int i = 0; i < 32; ++i) {
+            v[i] *= sl2;
+            mx = fmaxf(mx, v[i]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int key = key0 + i;
+            v[i] = (key < c1 && key <= qp) ? v[i] * sl2 : -INFINITY;
+            mx = fmaxf(mx, v[i]);
+          }
         }
         const float mn = fmaxf(run_m, mx);
         if (mn != -INFINITY) {
           float sum = 0.f;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sum += exp2f(v[i] - mn);
-          run_l = (run_m == -INFINITY ? 0.f : run_l * exp2f(run_m - mn)) + sum;
+          for (int i = 0; i < 32; ++i) sum += ex2(v[i] - mn);
+          run_l = (run_m == -INFINITY ? 0.f : run_l * ex2(run_m - mn)) + sum;
           run_m = mn;
         }
       }
@@ -198,8 +215,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(Geom g, const u
         tmem_ld32(taddr + cc * 32, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const int r = half * 64 + cc * 32 + i;
-          const float p = exp2f(v[i] * sl2 - ctl.rowm[r]) * ctl.rowil[r];
+          // p = 2^(s - m_r) / l_r = 2^(s - (m_r + log2 l_r)): one row constant per element
+          const float p = ex2(fmaf(v[i], sl2, -ctl.rowc[half * 64 + cc * 32 + i]));
           a1 += p;
           a2 += p * p;
         }
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(Geom g, const u
   for (int t = 0; t < n_tiles; ++t) {
     // K tile t landed (and Q): make the generic-proxy cp.async writes visible to the
     // tensor core's async proxy, then one thread issues the 8 K-steps of the MMA
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -235,10 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(Geom g, const u
       }
       mma_commit(&ctl.mbar[t & 1]);
     }
-    if (t >= 1) epilogue(t - 1);  // overlaps MMA t
-    // K buffer (t + 2) % 3 held tile t - 1, whose MMA has completed (epilogue waited on it)
-    if (t + 2 < n_tiles) load_k(t + 2);
-    asm volatile("cp.async.commit_group;\n");
+    if (t >= 1) epilogue(t - 1);  // overlaps MMA t; loads tile t + 1 into MMA t - 1's buffer
   }
   epilogue(n_tiles - 1);
 
