@@ -43,7 +43,7 @@ struct arkv_cache {
   int32_t* pcover = nullptr;
   bool persist = false;
   int num_sms = 148;
-  int jobs_per_wave = 0, max_splits = 64, n_chunks1_max = 1;
+  int jobs_per_wave = 0, jobs_per_prefill_wave = 0, max_splits = 64, n_chunks1_max = 1;
   // live kernel timing of the decode attention kernel (bench roofline)
   bool prof = false;
   std::vector<cudaEvent_t> ev;  // pairs
@@ -67,7 +67,7 @@ int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 struct Sizes {
   Geom g;
-  int n_spare, jobs_per_wave, max_splits, n_chunks1;
+  int n_spare, jobs_per_wave, jobs_scratch, max_splits, n_chunks1;
   int64_t arena, ws;
   int64_t off_meta, off_desc, off_err;
   int64_t w_partials, w_logits, w_st, w_src, w_pfp, w_accpf, w_oq, w_colsum, w_mstat, w_counters, w_plan, w_pparts;
@@ -133,7 +133,11 @@ Sizes compute_sizes(const arkv_config& c) {
   g.gamma = (float)c.gamma;
 
   s.n_spare = c.n_spare_slots > 0 ? c.n_spare_slots : g.batch * g.Hkv;
-  s.jobs_per_wave = std::min(s.n_spare, kMaxJobs);
+  s.jobs_per_wave = std::min(s.n_spare, kMaxJobs);  // decode tailors: one spare slot per job
+  // the prefill-end tailor writes every unit into its own (empty) slot: waves of up to
+  // kMaxJobs jobs, not bounded by the spares (measured: 32 waves of 8 units took 6 ms at
+  // configs[1])
+  s.jobs_scratch = std::max(s.jobs_per_wave, std::min(g.n_units, kMaxJobs));
   s.max_splits = c.max_splits > 0 ? c.max_splits : 64;
   s.n_chunks1 = (int)((c.max_prompt + kPfChunkHost - 1) / kPfChunkHost);
   const int n_slots = g.n_units + s.n_spare;
@@ -149,9 +153,9 @@ Sizes compute_sizes(const arkv_config& c) {
   w = round_up(w + (int64_t)g.n_units * g.G * (g.cap_o + g.cap_q) * 4, 256);
   s.w_st = w;
   const int64_t st_stride = std::max<int64_t>(g.max_pos, g.cap_o) + g.cap_q;
-  w = round_up(w + (int64_t)s.jobs_per_wave * st_stride, 256);
+  w = round_up(w + (int64_t)s.jobs_scratch * st_stride, 256);
   s.w_src = w;
-  w = round_up(w + (int64_t)s.jobs_per_wave * (g.cap_o + g.cap_q) * 4, 256);
+  w = round_up(w + (int64_t)s.jobs_scratch * (g.cap_o + g.cap_q) * 4, 256);
   s.w_pfp = w;
   w = round_up(w + (int64_t)g.n_units * s.n_chunks1 * g.G * g.W * 8, 256);
   s.w_accpf = w;
@@ -209,7 +213,10 @@ bool check_cuda(cudaError_t e) {
 
 extern "C" {
 
-const char* arkv_version(void) { return "arkv 0.1 sm_100a layouts=plain,frag kernels=generic,mma-sync-prefill"; }
+const char* arkv_version(void) {
+  return "arkv 0.2 sm_100a layouts=plain,frag decode=generic,mma-sync-split,mma-sync-persistent "
+         "prefill=tcgen05,mma-sync";
+}
 
 const char* arkv_status_string(arkv_status s) {
   switch (s) {
@@ -410,6 +417,7 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   c->pparts = (float*)(w + s.w_pparts);
   c->num_sms = prop.multiProcessorCount;
   c->jobs_per_wave = s.jobs_per_wave;
+  c->jobs_per_prefill_wave = s.jobs_scratch;
   c->max_splits = s.max_splits;
   c->n_chunks1_max = s.n_chunks1;
   const int BL = s.g.batch * s.g.L;
@@ -496,9 +504,10 @@ int32_t arkv_cache_info(const arkv_cache* c, int32_t what) {
 static arkv_status run_jobs(arkv_cache* c, std::vector<TailorJob>& jobs, const uint16_t* pk, const uint16_t* pv, int P,
                             cudaStream_t s) {
   const Geom& g = c->g;
+  const int wave = pk ? c->jobs_per_prefill_wave : c->jobs_per_wave;  // prefill jobs need no spare slot
   size_t i = 0;
   while (i < jobs.size()) {
-    const int n = (int)std::min<size_t>(jobs.size() - i, (size_t)c->jobs_per_wave);
+    const int n = (int)std::min<size_t>(jobs.size() - i, (size_t)wave);
     TailorJobs tj;
     std::memset(&tj, 0, sizeof(tj));
     int max_tiles = 1;
