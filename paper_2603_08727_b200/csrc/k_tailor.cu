@@ -11,6 +11,8 @@
 //          quantization with fp32 scale/zero in the oracle's operation order (R23),
 //          Quantized -> Quantized code copy (R25)), assembles the tile in shared
 //          memory and writes it out with coalesced 16-byte stores into a fresh slot.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace arkv {
@@ -481,6 +483,243 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
   for (int i = threadIdx.x * 16; i < tbytes; i += blockDim.x * 16) *(uint4*)(dst + i) = *(const uint4*)(tile + i);
 }
 
+// ---------------------------------------------------------------------------------
+// Move, FRAG layout / d = 128 / 4-bit (the paper's shapes): the 32 rows of a destination
+// tile are first materialised row-major in shared memory (16-byte loads for prompt rows
+// and for the K block of old Original tiles, whose 16-byte quads are 8 consecutive dims
+// of one token), quantised there when the tile is Quantized, and the tile is then
+// written straight to HBM one 16-byte quad per thread — each quad's contents come from
+// the FRAG maps of common.cuh specialised to d = 128 (no per-element layout arithmetic
+// on the store side).
+// ---------------------------------------------------------------------------------
+namespace mvf {
+constexpr int D = 128;
+constexpr int kRowH = D + 8;    // staged row stride in bf16 (pad: conflict-free transposed reads)
+constexpr int kRowC = D + 8;    // code row stride in bytes (8-byte aligned rows)
+struct Smem {
+  uint16_t stage[2][kTile][kRowH];  // K, V rows (bf16 bits)
+  uint8_t code[2][kTile][kRowC];    // K, V codes (Quantized tiles)
+  float4 sc[kTile][D / 16];         // per row and group: k_scale, k_zero, v_scale, v_zero (ng <= 8)
+};
+}  // namespace mvf
+
+template <int NG>
+__global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, TailorJobs jobs, uint8_t* slots,
+                                                               uint8_t* meta, const uint16_t* __restrict__ pk,
+                                                               const uint16_t* __restrict__ pv, int P,
+                                                               const int32_t* __restrict__ src_scratch,
+                                                               int src_stride) {
+  using namespace mvf;
+  __shared__ __align__(16) Smem sm;
+  griddep_wait();
+  Geom g = g_in;
+  g.d = D;
+  g.bits = 4;
+  g.ng = NG;
+  g.layout = ARKV_LAYOUT_FRAG;
+  constexpr int GS = D / NG;  // group size
+  const TailorJob jb = jobs.j[blockIdx.y];
+  const int n_o_new = jb.n_oe + jb.n_win_old;
+  const int tiles_o = (n_o_new + kTile - 1) / kTile;
+  const int tiles_q = (jb.n_q_new + kTile - 1) / kTile;
+  int tid = blockIdx.x;
+  if (tid >= tiles_o + tiles_q) return;
+  const bool dstQ = tid >= tiles_o;
+  if (dstQ) tid -= tiles_o;
+  const int32_t* src = src_scratch + (int64_t)blockIdx.y * src_stride + (dstQ ? g.cap_o : 0);
+  uint8_t* nslot = slots + (int64_t)jb.new_slot * g.slot_bytes;
+  const uint8_t* oslot = jb.old_slot >= 0 ? slots + (int64_t)jb.old_slot * g.slot_bytes : nullptr;
+  SlotMeta nm = slot_meta(meta, g, jb.new_slot);
+  SlotMeta om;
+  if (jb.old_slot >= 0) om = slot_meta(meta, g, jb.old_slot);
+  const uint16_t* upk = pk ? pk + (int64_t)jb.unit * P * D : nullptr;
+  const uint16_t* upv = pv ? pv + (int64_t)jb.unit * P * D : nullptr;
+  const int n_new = dstQ ? jb.n_q_new : n_o_new;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int off = g.mode == ARKV_QUANT_SYM ? 8 : 0;
+
+  // ---- phase 1: one warp per row ----
+  for (int j = warp; j < kTile; j += 8) {
+    const int row = tid * kTile + j;
+    if (row >= n_new) {  // rows past the segment: zeros (defined bytes; masked by the readers)
+      for (int i = lane; i < 2 * kRowH / 2; i += 32) ((uint32_t*)sm.stage[i / (kRowH / 2)][j])[i % (kRowH / 2)] = 0u;
+      if (dstQ) {
+        for (int i = lane; i < 2 * kRowC / 4; i += 32) ((uint32_t*)sm.code[i / (kRowC / 4)][j])[i % (kRowC / 4)] = 0u;
+        if (lane < NG) sm.sc[j][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      continue;
+    }
+    const int32_t sref = src[row];
+    const int kind = sref >> 28, orow = sref & 0x0FFFFFFF;
+    int pos;
+    if (kind == kSrcInput) pos = orow;
+    else if (kind == kSrcOldO) pos = om.pos_o[orow];
+    else pos = om.pos_q[orow];
+    if (lane == 0) {
+      if (dstQ) {
+        nm.pos_q[row] = pos;
+        nm.acc_q[row] = make_float2(0.f, 0.f);
+      } else {
+        nm.pos_o[row] = pos;
+        nm.acc_o[row] = make_float2(0.f, 0.f);
+      }
+    }
+    const int oj = orow & 31;
+    if (kind == kSrcOldQ) {
+      const uint8_t* qt = q_tile_ptr((uint8_t*)oslot, g, orow >> 5);
+      if (dstQ) {  // Q -> Q: keep codes and scales (R25)
+        for (int x = lane; x < D; x += 32) {
+          sm.code[0][j][x] = (uint8_t)read_code(g, qt, oj, x, false);
+          sm.code[1][j][x] = (uint8_t)read_code(g, qt, oj, x, true);
+        }
+        if (lane < NG) sm.sc[j][lane] = *(const float4*)(qt + q_sc_off(g, oj, 0, lane));
+        continue;
+      }
+      // Q -> O promotion (R24): bf16_rne(f32(f32(code * s) + z))
+      for (int x = lane; x < D; x += 32) {
+        const float4 s4 = *(const float4*)(qt + q_sc_off(g, oj, 0, x / GS));
+        const int ck = (int)read_code(g, qt, oj, x, false) - off;
+        const int cv = (int)read_code(g, qt, oj, x, true) - off;
+        sm.stage[0][j][x] = f_to_bf16_rne(__fadd_rn(__fmul_rn((float)ck, s4.x), s4.y));
+        sm.stage[1][j][x] = f_to_bf16_rne(__fadd_rn(__fmul_rn((float)cv, s4.z), s4.w));
+      }
+    } else if (kind == kSrcInput) {
+      // prompt row: 16 lanes x 16 B of K, 16 lanes x 16 B of V
+      const uint16_t* rowp = (lane < 16 ? upk : upv) + (int64_t)orow * D + (lane & 15) * 8;
+      *(uint4*)&sm.stage[lane >> 4][j][(lane & 15) * 8] = *(const uint4*)rowp;
+    } else {
+      // old Original row: K quad (t, q) holds dims 32t + 8q .. +7 of the token (FRAG K map)
+      const uint8_t* ot = o_tile_ptr((uint8_t*)oslot, g, orow >> 5);
+      const int mth = ((oj >> 4) << 1) | ((oj >> 3) & 1), gg = oj & 7;
+      if (lane < 16) {
+        const int t = lane >> 2, q = lane & 3;
+        *(uint4*)&sm.stage[0][j][32 * t + 8 * q] = *(const uint4*)(ot + ((mth * 4 + q) * 32 + 4 * gg + t) * 16);
+      }
+      for (int x = lane; x < D; x += 32) sm.stage[1][j][x] = *(const uint16_t*)(ot + o_v_off(g, oj, x));
+    }
+    if (!dstQ) continue;
+    // O -> Q: group quantisation (R23), fp32 op order identical to the oracle.  Lane owns
+    // dims 4 lane .. 4 lane + 3 (one group: g >= 4); the lanes of a group reduce together.
+    __syncwarp();
+    constexpr int LPG = GS / 4;  // lanes per group
+    float4 scv;                  // k_scale, k_zero, v_scale, v_zero of this lane's group
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint2 raw = *(const uint2*)&sm.stage[h][j][4 * lane];
+      const float xv[4] = {__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
+                           __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u)};
+      float mn = fminf(fminf(xv[0], xv[1]), fminf(xv[2], xv[3]));
+      float mx = fmaxf(fmaxf(xv[0], xv[1]), fmaxf(xv[2], xv[3]));
+      float am = fmaxf(fmaxf(fabsf(xv[0]), fabsf(xv[1])), fmaxf(fabsf(xv[2]), fabsf(xv[3])));
+#pragma unroll
+      for (int o = 1; o < LPG; o <<= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+      }
+      const bool sym = g.mode == ARKV_QUANT_SYM;
+      const bool flat = sym ? am == 0.f : mx == mn;
+      const float s = flat ? 1.f : (sym ? __fdiv_rn(am, 7.f) : __fdiv_rn(__fsub_rn(mx, mn), 15.f));
+      const float z = sym ? 0.f : mn;
+      // code = rint(f32(f32(x - z) / s)): the quotient through the reciprocal is within
+      // 3e-6 of the correctly rounded one (|q| <= 15), so it rounds to the same integer
+      // unless it lies within 1e-5 of a half-integer — then the exact division decides
+      const float r = __frcp_rn(s);
+      const bool tiny = s < 1e-30f;
+      uint32_t word = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float num = sym ? xv[e] : __fsub_rn(xv[e], mn);
+        float q = __fmul_rn(num, r);
+        if (tiny || fabsf(q - floorf(q) - 0.5f) < 1e-5f) q = __fdiv_rn(num, s);
+        int c = __float2int_rn(q);
+        c = flat ? 0 : (sym ? max(-7, min(7, c)) : max(0, min(15, c)));
+        word |= (uint32_t)((c + off) & 0xFF) << (8 * e);
+      }
+      *(uint32_t*)&sm.code[h][j][4 * lane] = word;
+      if (h == 0) {
+        scv.x = s;
+        scv.y = z;
+      } else {
+        scv.z = s;
+        scv.w = z;
+      }
+    }
+    if (lane % LPG == 0) sm.sc[j][lane / LPG] = scv;
+  }
+  __syncthreads();
+
+  // ---- phase 2: 16-byte output quads straight to HBM ----
+  if (!dstQ) {
+    uint8_t* dst = o_tile_ptr(nslot, g, tid);
+    for (int i = threadIdx.x; i < 2 * 512; i += 256) {
+      const int qd = i & 511, ql = qd & 31, kq = qd >> 5;  // quad index = (k >> 2) * 32 + lane
+      const int gg = ql >> 2, t = ql & 3;
+      uint4 v;
+      if (i < 512) {
+        // K block: kq = mth * 4 + q -> token mth*8 + gg (mth = 2mt + h), dims 32t + 8q .. +7
+        const int j = (kq >> 2) * 8 + gg, q = kq & 3;
+        v = *(const uint4*)&sm.stage[0][j][32 * t + 8 * q];
+      } else {
+        // V^T block: kq = mtv * 2 + kc; word (sel, hi) = dim 16mtv + 8sel + gg, tokens
+        // 16kc + 8hi + 2t + {0, 1}
+        const int mtv = kq >> 1, kc = kq & 1;
+        uint32_t w[4];
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi)
+#pragma unroll
+          for (int sel = 0; sel < 2; ++sel) {
+            const int x = 16 * mtv + 8 * sel + gg, j0 = 16 * kc + 8 * hi + 2 * t;
+            w[sel + 2 * hi] = (uint32_t)sm.stage[1][j0][x] | ((uint32_t)sm.stage[1][j0 + 1][x] << 16);
+          }
+        v = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      *(uint4*)(dst + (i < 512 ? 0 : 64 * D) + (int64_t)qd * 16) = v;
+    }
+  } else {
+    uint8_t* dst = q_tile_ptr(nslot, g, tid);
+    // code blocks: 2 x 128 quads (K block 16 d bytes, V block 16 d bytes)
+    for (int i = threadIdx.x; i < 256; i += 256) {
+      const int isv = i >> 7, qd = i & 127, ql = qd & 31, kq = qd >> 5;
+      const int gg = ql >> 2, t = ql & 3;
+      uint32_t w[4];
+      if (!isv) {
+        // K codes: word k = mth * 4 + jp (kq = mth), nibble e = dim 32jp + 8t + e of token mth*8 + gg
+        const int j = kq * 8 + gg;
+#pragma unroll
+        for (int jp = 0; jp < 4; ++jp) {
+          const uint2 c8 = *(const uint2*)&sm.code[0][j][32 * jp + 8 * t];
+          uint32_t a = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a |= ((c8.x >> (8 * e)) & 0xFu) << (4 * e);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) a |= ((c8.y >> (8 * e)) & 0xFu) << (4 * (e + 4));
+          w[jp] = a;
+        }
+      } else {
+        // V codes: word k = mtv * 2 + sel (kq = mtv), dim 16mtv + 8sel + gg; nibble e = 2kc +
+        // hi + 4u holds token 16kc + 8hi + 2t + u
+#pragma unroll
+        for (int wi = 0; wi < 4; ++wi) {
+          const int k = kq * 4 + wi, mtv = k >> 1, sel = k & 1;
+          const int x = 16 * mtv + 8 * sel + gg;
+          uint32_t a = 0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int kc = (e >> 1) & 1, hi = e & 1, u = e >> 2;
+            a |= ((uint32_t)sm.code[1][16 * kc + 8 * hi + 2 * t + u][x] & 0xFu) << (4 * e);
+          }
+          w[wi] = a;
+        }
+      }
+      *(uint4*)(dst + isv * 16 * D + (int64_t)qd * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    // scales: [row][group] quads after the codes
+    for (int i = threadIdx.x; i < kTile * NG; i += 256)
+      *(float4*)(dst + 32 * D + i * 16) = sm.sc[i / NG][i % NG];
+  }
+}
+
 int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_tiles, uint8_t* slots, uint8_t* meta,
                   UnitDesc* desc, const uint16_t* pk, const uint16_t* pv, int P, const float2* acc_pf,
                   int8_t* st_scratch, int32_t* src_scratch, int32_t* err, cudaStream_t s) {
@@ -489,8 +728,21 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
   launch_pdl(tailor_select_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, meta, acc_pf, st_scratch, st_stride);
   launch_pdl(tailor_scan_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, desc, (const int8_t*)st_scratch, st_stride,
              src_scratch, src_stride, err);
-  size_t smem = (size_t)max(g.tile_o, ((g.tile_q + 15) & ~15) + 2 * kTile * g.d);
   dim3 grid(max_tiles, n_jobs);
+  if (g.layout == ARKV_LAYOUT_FRAG && g.d == mvf::D && g.bits == 4 && std::getenv("ARKV_MOVE_GENERIC") == nullptr) {
+    switch (g.ng) {
+      case 1: launch_pdl(tailor_move_frag_kernel<1>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
+                         (const int32_t*)src_scratch, src_stride); return 3;
+      case 2: launch_pdl(tailor_move_frag_kernel<2>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
+                         (const int32_t*)src_scratch, src_stride); return 3;
+      case 4: launch_pdl(tailor_move_frag_kernel<4>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
+                         (const int32_t*)src_scratch, src_stride); return 3;
+      case 8: launch_pdl(tailor_move_frag_kernel<8>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
+                         (const int32_t*)src_scratch, src_stride); return 3;
+      default: break;
+    }
+  }
+  size_t smem = (size_t)max(g.tile_o, ((g.tile_q + 15) & ~15) + 2 * kTile * g.d);
   const int vpl = (g.d + 31) / 32;
 #define MV_LAUNCH(V, DCV)                                                                                         \
   cudaFuncSetAttribute(tailor_move_kernel<V, DCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \

@@ -345,3 +345,74 @@ def test_full_size_configs1_sampled_units():
             np.testing.assert_array_equal(e["q_k"][qm], r["q_k"][qm])
             np.testing.assert_array_equal(e["k_zero"][qm], r["k_zero"][qm])
         assert full >= 2, f"layer {l}: fewer than two units with a score margin"
+
+
+def _sampled_units_run(sh, budget, steps, seqs, layers, recipe, seed, decode_kernel=0):
+    """Run a full-size cache for `steps` decode steps (bench launch: one call for all
+    layers) and compare sampled (sequence, layer) slices with per-slice oracles."""
+    from paper_2603_08727_b200 import arkv as A
+    from synth import prefill_inputs_fast, decode_inputs_fast, prefill_inputs_margin_fast, decode_inputs_margin_fast
+    pf = prefill_inputs_margin_fast if recipe == "margin" else prefill_inputs_fast
+    df = decode_inputs_margin_fast if recipe == "margin" else decode_inputs_fast
+    cfg = A.make_config(sh.n_layers, sh.n_q_heads, sh.n_kv_heads, sh.head_dim, batch=sh.batch, window=sh.window,
+                        budget_tokens=budget, max_positions=sh.prompt_len + steps + 1, max_prompt=sh.prompt_len,
+                        decode_kernel=decode_kernel)
+    gpu = A.ArkvCache(cfg)
+    qw, k, v = pf(sh, seed=seed, device="cuda")
+    stats, oq, rho = gpu.arkv_prefill_stats(qw, k, v)
+    gpu.arkv_check()
+    ocfg = O.Cfg(n_layers=1, n_q_heads=sh.n_q_heads, n_kv_heads=sh.n_kv_heads, head_dim=sh.head_dim,
+                 window=sh.window, budget_tokens=budget)
+    oras = {}
+    for b in seqs:
+        for l in layers:
+            ora = O.OracleARKV(ocfg)
+            sub = lambda t: t[b:b + 1, l:l + 1].double().cpu().numpy()   # noqa: E731
+            ora.prefill(sub(qw), sub(k), sub(v), rho_override=[[rho[b, l]]])
+            oras[(b, l)] = ora
+    del qw, k, v
+    for s in range(steps):
+        q, kn, vn = df(sh, s, seed=seed, device="cuda")
+        out = gpu.arkv_decode_step(q, kn, vn, out_fp32=True).cpu().numpy()
+        for (b, l), ora in oras.items():
+            ref = ora.decode_step(q[b:b + 1, l:l + 1].double().cpu().numpy(), kn[b:b + 1, l:l + 1].double().cpu().numpy(),
+                                  vn[b:b + 1, l:l + 1].double().cpu().numpy())
+            np.testing.assert_allclose(out[b:b + 1, l:l + 1], ref, rtol=RTOL, atol=ATOL, err_msg=f"b{b} l{l} step {s}")
+    gpu.arkv_check()
+    checked = 0
+    for (b, l), ora in oras.items():
+        for h in range(sh.n_kv_heads):
+            e, r = gpu.arkv_export_unit(b, l, h), ora.export(0, 0, h)
+            assert (e["n_o"], e["n_q"]) == (r["n_o"], r["n_q"])
+            margins = ora.units[(0, 0, h)].margins
+            if margins and min(margins) <= MARGIN:
+                continue
+            checked += 1
+            np.testing.assert_array_equal(e["state"], r["state"])
+            om, qm = r["state"] == 1, r["state"] == 2
+            np.testing.assert_array_equal(_bf16_bits_to_f64(e["o_v"])[om], r["o_v"][om])
+            np.testing.assert_array_equal(e["q_k"][qm], r["q_k"][qm])
+            np.testing.assert_array_equal(e["v_scale"][qm], r["v_scale"][qm])
+    return checked, oras
+
+
+@pytest.mark.parametrize("kernel", [2, 3])
+def test_full_size_configs3_short_prompts(kernel):
+    """configs[3] at full size (batch 64 x 32 layers x 8 KV heads, 1K prompts, B = 2048: the
+    full-precision-matching regime, no tailor): sampled sequences and layers vs the oracle."""
+    sh = Shape(batch=64, n_layers=32, n_q_heads=32, n_kv_heads=8, head_dim=128, prompt_len=1024, window=32)
+    checked, oras = _sampled_units_run(sh, 2048, 24, seqs=[0, 37, 63], layers=[0, 31], recipe="natural", seed=29,
+                                       decode_kernel=kernel)
+    assert checked == 3 * 2 * 8
+    assert all(len(u.tailors) == 0 for o in oras.values() for u in o.units.values())
+
+
+@pytest.mark.parametrize("kernel", [2, 3])
+def test_full_size_configs2_batch8(kernel):
+    """configs[2]'s per-GPU shard at full size (Qwen3-8B: 36 layers, batch 8, 8K prompts,
+    B = 2048): prefill-end tailor on every unit; sampled units vs the oracle."""
+    sh = Shape(batch=8, n_layers=36, n_q_heads=32, n_kv_heads=8, head_dim=128, prompt_len=8192, window=32)
+    checked, oras = _sampled_units_run(sh, 2048, 40, seqs=[0, 5], layers=[3, 30], recipe="margin", seed=31,
+                                       decode_kernel=kernel)
+    assert checked >= 8
+    assert all(len(u.tailors) >= 1 for o in oras.values() for u in o.units.values())
