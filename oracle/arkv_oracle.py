@@ -39,7 +39,8 @@ class Cfg:
     budget_tokens: int = 512         # B in bf16-token equivalents per (seq, layer, kv head) (R10, R11)
     quant_bits: int = 4              # R23
     group_size: int = 0              # 0 -> head_dim ("per-token scale")
-    quant_mode: str = "asym"         # "asym" (scale, zero=min) | "sym"
+    quant_mode: str = "asym"         # "asym" (scale, zero=min) | "sym" |
+                                     # "fp8" (e4m3 codes, per-group scale: P:333; NEXT-2)
     alpha: float = 0.75
     tau: Tuple[float, float, float] = (7.774, 5.407, 5.528)
     gamma: float = 263.81
@@ -73,8 +74,10 @@ def validate(cfg: Cfg) -> None:
         raise ValueError("head_dim*bits must be a whole number of bytes")
     if cfg.budget_tokens <= 2 * cfg.window:
         raise ValueError("budget must exceed 2W (R14)")
-    if cfg.quant_mode not in ("asym", "sym"):
+    if cfg.quant_mode not in ("asym", "sym", "fp8"):
         raise ValueError("quant_mode")
+    if cfg.quant_mode == "fp8" and cfg.quant_bits != 8:
+        raise ValueError("fp8 codes are 8 bits")
 
 
 # ----------------------------------------------------------------------------
@@ -298,6 +301,8 @@ def quantize(x: np.ndarray, bits: int, g: int, mode: str = "asym"):
             code = clamp(rint_even(f32(f32(x-mn)/s)), 0, 2^b-1); constant group: s=1, codes 0.
       sym:  a = max|x|; s = f32(a / f32(2^(b-1)-1)); z = 0;
             code = clamp(rint_even(f32(x/s)), ±(2^(b-1)-1)); zero group: s=1, codes 0.
+      fp8:  a = max|x|; s = f32(a / 448); z = 0; code = e4m3_rne_satfinite(f32(x/s))
+            (byte, NEXT-2); zero group: s=1, codes 0x00.
     Returns (codes int64[d], scale f32[d/g], zero f32[d/g])."""
     xf = np.asarray(x, dtype=np.float64).astype(F32)
     d = xf.shape[0]
@@ -317,6 +322,15 @@ def quantize(x: np.ndarray, bits: int, g: int, mode: str = "asym"):
                 # float32 array ops round each element exactly like the scalar ops
                 c = np.rint((xs - mn).astype(F32) / s).astype(np.int64)
                 c = np.clip(c, 0, 2 ** bits - 1)
+        elif mode == "fp8":
+            # per-group scale s = f32(a / 448) with a = max|x|; code = e4m3(f32(x / s))
+            a = F32(np.abs(xs).max())
+            if a == 0:
+                s, z, c = F32(1.0), F32(0.0), np.zeros(g, dtype=np.int64)
+            else:
+                s = F32(a / F32(E4M3_MAX))
+                z = F32(0.0)
+                c = e4m3_encode((xs / s).astype(F32))
         else:
             a = F32(np.abs(xs).max())
             qmax = 2 ** (bits - 1) - 1
@@ -333,12 +347,50 @@ def quantize(x: np.ndarray, bits: int, g: int, mode: str = "asym"):
     return codes, sc, zr
 
 
-def dequantize(codes: np.ndarray, scale: np.ndarray, zero: np.ndarray, g: int) -> np.ndarray:
+# ---- OCP FP8 E4M3 ("FP8"): 1 sign, 4 exponent bits (bias 7), 3 mantissa
+# bits; no infinities; S.1111.111 is NaN, so the largest finite magnitude is 448 ----
+def _e4m3_magnitudes() -> np.ndarray:
+    v = np.empty(127)
+    for c in range(127):
+        e, m = c >> 3, c & 7
+        v[c] = (m / 8.0) * 2.0 ** -6 if e == 0 else (1.0 + m / 8.0) * 2.0 ** (e - 7)
+    return v
+
+
+E4M3 = _e4m3_magnitudes()       # magnitude of codes 0x00..0x7E, strictly increasing
+E4M3_MAX = 448.0
+
+
+def e4m3_encode(x) -> np.ndarray:
+    """float32 values -> e4m3 code bytes: round to nearest, ties to the even code,
+    magnitudes above 448 saturate to 448 ("satfinite"); the sign bit is kept (-0 -> 0x80)."""
+    xf = np.asarray(x, dtype=F32).astype(np.float64)
+    a = np.minimum(np.abs(xf), E4M3_MAX)
+    hi = np.searchsorted(E4M3, a, side="left")          # first magnitude >= a
+    hi = np.minimum(hi, 126)
+    lo = np.maximum(hi - 1, 0)
+    dlo, dhi = a - E4M3[lo], E4M3[hi] - a
+    pick_lo = (dlo < dhi) | ((dlo == dhi) & (lo % 2 == 0))
+    c = np.where(E4M3[hi] == a, hi, np.where(pick_lo, lo, hi)).astype(np.int64)
+    return c | (np.signbit(xf).astype(np.int64) << 7)
+
+
+def e4m3_decode(codes) -> np.ndarray:
+    c = np.asarray(codes, dtype=np.int64)
+    return np.where(c & 0x80, -1.0, 1.0) * E4M3[c & 0x7F]
+
+
+def code_values(codes: np.ndarray, mode: str) -> np.ndarray:
+    """The number a stored code stands for: the integer itself, or the e4m3 value."""
+    return e4m3_decode(codes) if mode == "fp8" else np.asarray(codes, dtype=np.float64)
+
+
+def dequantize(codes: np.ndarray, scale: np.ndarray, zero: np.ndarray, g: int, mode: str = "asym") -> np.ndarray:
     """Alg. 1: x̃ = q̂·s (+ z for the asymmetric zero point), evaluated
     in float64 from the fp32 scale and zero — the values attention sees (R23)."""
     s = np.repeat(np.asarray(scale, dtype=np.float64), g)
     z = np.repeat(np.asarray(zero, dtype=np.float64), g)
-    return np.asarray(codes, dtype=np.float64) * s + z
+    return code_values(codes, mode) * s + z
 
 
 def f32_to_bf16_rne(x: np.ndarray) -> np.ndarray:
@@ -348,13 +400,15 @@ def f32_to_bf16_rne(x: np.ndarray) -> np.ndarray:
     return r.astype(np.uint32).view(F32).astype(np.float64).reshape(np.shape(x))
 
 
-def promote(codes: np.ndarray, scale: np.ndarray, zero: np.ndarray, g: int) -> np.ndarray:
-    """Q -> O re-materialisation (R24): bf16_rne(f32(f32(code·s) + z)), per element."""
+def promote(codes: np.ndarray, scale: np.ndarray, zero: np.ndarray, g: int, mode: str = "asym") -> np.ndarray:
+    """Q -> O re-materialisation (R24): bf16_rne(f32(f32(code·s) + z)), per element
+    (code = its e4m3 value in fp8 mode)."""
     d = len(codes)
+    cv = code_values(codes, mode)
     out = np.empty(d, dtype=F32)
     for i in range(d):
         gi = i // g
-        out[i] = F32(F32(F32(codes[i]) * scale[gi]) + zero[gi])
+        out[i] = F32(F32(F32(cv[i]) * scale[gi]) + zero[gi])
     return f32_to_bf16_rne(out)
 
 
@@ -439,8 +493,11 @@ class UnitCache:
         segment; the order does not affect attention (R26)."""
         g = self.cfg.group_size
         # dequantize() applied to every Quantized row (vectorised over rows)
-        qk = self.q_kc * np.repeat(self.q_ks.astype(np.float64), g, axis=1) + np.repeat(self.q_kz.astype(np.float64), g, axis=1)
-        qv = self.q_vc * np.repeat(self.q_vs.astype(np.float64), g, axis=1) + np.repeat(self.q_vz.astype(np.float64), g, axis=1)
+        mode = self.cfg.quant_mode
+        qk = code_values(self.q_kc, mode) * np.repeat(self.q_ks.astype(np.float64), g, axis=1) + \
+            np.repeat(self.q_kz.astype(np.float64), g, axis=1)
+        qv = code_values(self.q_vc, mode) * np.repeat(self.q_vs.astype(np.float64), g, axis=1) + \
+            np.repeat(self.q_vz.astype(np.float64), g, axis=1)
         pos = np.concatenate([self.o_pos, self.q_pos])
         return pos, np.vstack([self.o_k, qk]), np.vstack([self.o_v, qv])
 
@@ -494,8 +551,8 @@ class UnitCache:
             s = new_state[p]
             if s == 1:
                 o_pos.append(p)
-                o_k.append(promote(self.q_kc[i], self.q_ks[i], self.q_kz[i], g))
-                o_v.append(promote(self.q_vc[i], self.q_vs[i], self.q_vz[i], g))
+                o_k.append(promote(self.q_kc[i], self.q_ks[i], self.q_kz[i], g, mode))
+                o_v.append(promote(self.q_vc[i], self.q_vs[i], self.q_vz[i], g, mode))
             elif s == 2:
                 q_pos.append(p); q_kc.append(self.q_kc[i]); q_vc.append(self.q_vc[i])
                 q_ks.append(self.q_ks[i]); q_kz.append(self.q_kz[i]); q_vs.append(self.q_vs[i]); q_vz.append(self.q_vz[i])
