@@ -165,6 +165,7 @@ def run_arkv(args, wl):
         budget = P + total_steps + 2 * wl["window"] + 1
     cfg = A.make_config(L, Hq, Hkv, d, batch=B, window=wl["window"], budget_tokens=budget,
                         quant_bits=wl["bits"], group_size=wl["group"], max_positions=P + total_steps + 1,
+                        quant_mode={"asym": A.QUANT_ASYM, "fp8": A.QUANT_FP8}[wl["qmode"]],
                         max_prompt=P, decode_kernel=args.kernel)
     cache = A.ArkvCache(cfg, dev)
     sh = Shape(batch=B, n_layers=L, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, prompt_len=P, window=wl["window"])
@@ -321,12 +322,13 @@ def run_arkv(args, wl):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "bf16+int4 (fp32 accumulate)",
+        "dtype": "bf16+int4 (fp32 accumulate)" if wl["qmode"] == "asym" else "bf16+fp8e4m3 (fp32 accumulate)",
         "data": "synthetic (synth/ natural recipe: sinks, 5% log-normal heavy hitters, recency bump, x8 outlier V channels)",
         "config": {"workload": f"{args.workload} (BASELINE.json configs[{wl['baseline_cfg']}])",
                    "layers": L, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d, "batch_per_gpu": B,
                    "global_batch": B * ws, "prompt_len": P, "budget_tokens": budget, "window": wl["window"], "mode": args.mode,
-                   "quant": f"int{wl['bits']} g{wl['group']} asym", "alpha": 0.75,
+                   "quant": (f"int{wl['bits']} g{wl['group']} asym" if wl["qmode"] == "asym"
+                             else f"fp8 e4m3 g{wl['group']}"), "alpha": 0.75,
                    "launch": "one arkv_decode_step per step covering all layers (layer-batched)",
                    "decode_kernel": cache_kernel(cache),
                    "parallelism": f"dp{ws} (whole sequences per GPU, no collective in the loop)",
@@ -404,7 +406,7 @@ def cpu_baseline(wl, rho_seq, samples=4):
     sh1 = Shape(batch=1, n_layers=L, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, prompt_len=P, window=wl["window"])
     qw, k, v = prefill_inputs_fast(sh1, seed=1234, device="cpu")
     cfg = O.Cfg(n_layers=1, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, window=wl["window"], budget_tokens=wl["budget"],
-                quant_bits=wl["bits"], group_size=wl["group"])
+                quant_bits=wl["bits"], group_size=wl["group"], quant_mode=wl.get("qmode", "asym"))
     ora = O.OracleARKV(cfg)
     f = lambda t: t.double().numpy()  # noqa: E731
     ora.prefill(f(qw[:, li:li + 1]), f(k[:, li:li + 1]), f(v[:, li:li + 1]), rho_override=[[r]])
@@ -438,7 +440,7 @@ def run_reference(args, wl):
     qw, k, v = prefill_inputs_fast(sh1, seed=1234, device="cpu")
     li = L // 2
     cfg = O.Cfg(n_layers=1, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, window=wl["window"], budget_tokens=wl["budget"],
-                quant_bits=wl["bits"], group_size=wl["group"])
+                quant_bits=wl["bits"], group_size=wl["group"], quant_mode=wl.get("qmode", "asym"))
     ora = O.OracleARKV(cfg)
     f = lambda t: t.double().numpy()  # noqa: E731
     ora.prefill(f(qw[:, li:li + 1]), f(k[:, li:li + 1]), f(v[:, li:li + 1]), rho_override=[[0.6]])
@@ -481,6 +483,8 @@ def main():
                     help="arkv (stats-driven rho) or the paper's baselines: base, origin (rho=1), quant (rho=0)")
     ap.add_argument("--prompt-len", type=int, default=0, help="debug: override the workload's prompt length")
     ap.add_argument("--layers", type=int, default=0, help="debug: override the workload's layer count")
+    ap.add_argument("--quant", default="int4", choices=["int4", "fp8"],
+                    help="Q-token format: int4 g128 asymmetric (default) or fp8 e4m3 per-token scale (NEXT-2)")
     args = ap.parse_args()
     if args.e2e_steps < 0:
         args.e2e_steps = args.steps
@@ -489,6 +493,9 @@ def main():
         wl["prompt_len"] = args.prompt_len
     if args.layers:
         wl["n_layers"] = args.layers
+    wl["qmode"] = "asym"
+    if args.quant == "fp8":
+        wl.update(bits=8, group=wl["head_dim"], qmode="fp8")
     if args.impl == "reference":
         args.steps = min(args.steps, 128)   # each step is a bounded CPU sample (one layer-step)
         args.warmup = min(args.warmup, 4)

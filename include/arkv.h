@@ -53,8 +53,10 @@ typedef enum {
 
 /* Layout of the tiles in HBM. */
 enum { ARKV_LAYOUT_AUTO = 0, ARKV_LAYOUT_PLAIN = 1, ARKV_LAYOUT_FRAG = 2 };
-/* Quantization mode (R23). */
-enum { ARKV_QUANT_ASYM = 0, ARKV_QUANT_SYM = 1 };
+/* Quantization mode (R23).  ARKV_QUANT_FP8 (NEXT-2; the paper's FP8 Q tokens, P:333,
+   P:486): quant_bits = 8, each code is an OCP e4m3 byte, per-group fp32 scale
+   s = max|x| / 448 (zero slot kept, always 0); code = e4m3_rne_satfinite(f32(x / s)). */
+enum { ARKV_QUANT_ASYM = 0, ARKV_QUANT_SYM = 1, ARKV_QUANT_FP8 = 2 };
 
 typedef struct arkv_config {
   int32_t n_layers;      /* L */
@@ -67,7 +69,7 @@ typedef struct arkv_config {
                             B_bytes = B * 4 * d (Eq. 1 in bytes, R10, R11) */
   int32_t quant_bits;    /* 2 | 4 | 8 (R23) */
   int32_t group_size;    /* g, divides d (0 -> d, "per-token scale") */
-  int32_t quant_mode;    /* ARKV_QUANT_ASYM (scale, zero=min) | ARKV_QUANT_SYM */
+  int32_t quant_mode;    /* ARKV_QUANT_ASYM (scale, zero=min) | ARKV_QUANT_SYM | ARKV_QUANT_FP8 */
   int32_t max_positions; /* prompt + decode steps upper bound */
   int32_t max_prompt;    /* largest prompt_len passed to arkv_prefill_stats */
   int32_t layout;        /* ARKV_LAYOUT_* (AUTO: FRAG when d % 32 == 0 and bits == 4) */

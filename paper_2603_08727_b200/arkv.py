@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libarkv.so")
 
 LAYOUT_AUTO, LAYOUT_PLAIN, LAYOUT_FRAG = 0, 1, 2
-QUANT_ASYM, QUANT_SYM = 0, 1
+QUANT_ASYM, QUANT_SYM, QUANT_FP8 = 0, 1, 2
 
 
 class ArkvConfig(ctypes.Structure):

@@ -91,7 +91,9 @@ arkv_status validate(const arkv_config* c) {
   int gs = c->group_size ? c->group_size : c->head_dim;
   if (gs < 8 || gs % 8 || c->head_dim % gs) return ARKV_ERR_CONFIG;
   if (c->budget_tokens <= 2 * c->window) return ARKV_ERR_CONFIG;  // R14
-  if (c->quant_mode != ARKV_QUANT_ASYM && c->quant_mode != ARKV_QUANT_SYM) return ARKV_ERR_CONFIG;
+  if (c->quant_mode != ARKV_QUANT_ASYM && c->quant_mode != ARKV_QUANT_SYM && c->quant_mode != ARKV_QUANT_FP8)
+    return ARKV_ERR_CONFIG;
+  if (c->quant_mode == ARKV_QUANT_FP8 && c->quant_bits != 8) return ARKV_ERR_CONFIG;
   if (c->max_positions <= 0 || c->max_prompt <= 0 || c->max_prompt > c->max_positions) return ARKV_ERR_CONFIG;
   if (c->alpha <= 0.0 || c->alpha > 1.0) return ARKV_ERR_CONFIG;
   if (c->layout == ARKV_LAYOUT_FRAG && (c->quant_bits != 4 || c->head_dim % 32)) return ARKV_ERR_CONFIG;

@@ -19,6 +19,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <stdint.h>
 
 #include "../../include/arkv.h"
@@ -194,6 +196,16 @@ __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wa
 __device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 __device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+
+// The number a stored Quantized code stands for (R23): the integer (minus the symmetric
+// offset), or the e4m3 value of an fp8 code (NEXT-2).
+__device__ __forceinline__ float code_value(const Geom& g, uint32_t raw) {
+  if (g.mode == ARKV_QUANT_FP8) {
+    const __half_raw h = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)raw, __NV_E4M3);
+    return __half2float(__half(h));
+  }
+  return (float)((int)raw - (g.mode == ARKV_QUANT_SYM ? (1 << (g.bits - 1)) : 0));
+}
 __device__ __forceinline__ uint16_t f_to_bf16_rne(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }

@@ -102,7 +102,6 @@ __global__ void __launch_bounds__(128) decode_split_generic(DecodeArgs a) {
     }
   }
 
-  const int off = g.mode == ARKV_QUANT_SYM ? (1 << (g.bits - 1)) : 0;
   const int n_work = (o1 - o0) + (q1 - q0);
   for (int wi = warp; wi < n_work; wi += 4) {
     const bool isq = wi >= (o1 - o0);
@@ -138,11 +137,11 @@ __global__ void __launch_bounds__(128) decode_split_generic(DecodeArgs a) {
           for (int i = 0; i < 8; ++i) {
             int byte, shift;
             q_k_loc(g, j, x0 + i, &byte, &shift);
-            int ck = (int)((tb[byte] >> shift) & ((1u << g.bits) - 1u)) - off;
+            const float ck = code_value(g, (tb[byte] >> shift) & ((1u << g.bits) - 1u));
             q_v_loc(g, j, x0 + i, &byte, &shift);
-            int cv = (int)((tb[byte] >> shift) & ((1u << g.bits) - 1u)) - off;
-            kf[i] = (float)ck * ks + kz;
-            vf[i] = (float)cv * vs + vz;
+            const float cv = code_value(g, (tb[byte] >> shift) & ((1u << g.bits) - 1u));
+            kf[i] = ck * ks + kz;
+            vf[i] = cv * vs + vz;
           }
         }
       }

@@ -400,10 +400,10 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
           float kz = *(const float*)(qt + q_sc_off(g, oj, 1, grp));
           float vs = *(const float*)(qt + q_sc_off(g, oj, 2, grp));
           float vz = *(const float*)(qt + q_sc_off(g, oj, 3, grp));
-          int ck = (int)read_code(g, qt, oj, x, false) - off;
-          int cv = (int)read_code(g, qt, oj, x, true) - off;
-          kx = bf16_to_f(f_to_bf16_rne(__fadd_rn(__fmul_rn((float)ck, ks), kz)));
-          vx = bf16_to_f(f_to_bf16_rne(__fadd_rn(__fmul_rn((float)cv, vs), vz)));
+          const float ck = code_value(g, read_code(g, qt, oj, x, false));
+          const float cv = code_value(g, read_code(g, qt, oj, x, true));
+          kx = bf16_to_f(f_to_bf16_rne(__fadd_rn(__fmul_rn(ck, ks), kz)));
+          vx = bf16_to_f(f_to_bf16_rne(__fadd_rn(__fmul_rn(cv, vs), vz)));
         }
       }
       kvv[0][t] = kx;
@@ -441,7 +441,11 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
         }
         float s, z;
         bool flat;
-        if (g.mode == ARKV_QUANT_SYM) {
+        if (g.mode == ARKV_QUANT_FP8) {  // NEXT-2: s = f32(max|x| / 448), z = 0
+          flat = am == 0.f;
+          s = flat ? 1.f : __fdiv_rn(am, 448.f);
+          z = 0.f;
+        } else if (g.mode == ARKV_QUANT_SYM) {
           flat = am == 0.f;
           s = flat ? 1.f : __fdiv_rn(am, (float)qmaxv);
           z = 0.f;
@@ -457,6 +461,8 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
             int c;
             if (flat) {
               c = 0;
+            } else if (g.mode == ARKV_QUANT_FP8) {  // e4m3 byte: RNE, satfinite
+              c = (int)__nv_cvt_float_to_fp8(__fdiv_rn(kvv[kv][t], s), __NV_SATFINITE, __NV_E4M3);
             } else if (g.mode == ARKV_QUANT_SYM) {
               c = __float2int_rn(__fdiv_rn(kvv[kv][t], s));
               c = max(-qmaxv, min(qmaxv, c));

@@ -50,8 +50,14 @@ def test_config_validation():
     c = A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, layout=A.LAYOUT_FRAG)  # d % 32 != 0
     with pytest.raises(A.ArkvError):
         A.arkv_cache_bytes(c)
+    c = A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, quant_bits=4, quant_mode=A.QUANT_FP8)  # fp8 is 8-bit
+    with pytest.raises(A.ArkvError):
+        A.arkv_cache_bytes(c)
     a, w = A.arkv_cache_bytes(A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, max_positions=128))
     assert a > 0 and w > 0
+    a8, _ = A.arkv_cache_bytes(A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, max_positions=128,
+                                             quant_bits=8, quant_mode=A.QUANT_FP8))
+    assert a8 > 0
 
 
 def test_arena_respects_budget():

@@ -46,7 +46,7 @@ def make_pair(sh: Shape, budget, bits=4, g=0, mode="asym", layout=0, steps=64, d
     from paper_2603_08727_b200 import arkv as A
     cfg = A.make_config(sh.n_layers, sh.n_q_heads, sh.n_kv_heads, sh.head_dim, batch=sh.batch, window=sh.window,
                         budget_tokens=budget, quant_bits=bits, group_size=g,
-                        quant_mode=A.QUANT_SYM if mode == "sym" else A.QUANT_ASYM,
+                        quant_mode={"asym": A.QUANT_ASYM, "sym": A.QUANT_SYM, "fp8": A.QUANT_FP8}[mode],
                         max_positions=sh.prompt_len + steps + 1, max_prompt=sh.prompt_len, layout=layout,
                         decode_kernel=decode_kernel, max_splits=max_splits, n_spare_slots=n_spare)
     gpu = A.ArkvCache(cfg, "cuda")
@@ -129,6 +129,8 @@ MID = Shape(batch=1, n_layers=2, n_q_heads=8, n_kv_heads=2, head_dim=128, prompt
     (1, 2, 32, "asym"),
     (1, 8, 128, "sym"),
     (2, 4, 64, "sym"),
+    (1, 8, 128, "fp8"),    # NEXT-2: e4m3 codes, per-token scale
+    (1, 8, 32, "fp8"),
 ])
 def test_mid_config(layout, bits, g, mode):
     """L=2, H_q=8, H_kv=2, d=128, P=2048, B=512: prefill tailor + decode tailors."""
