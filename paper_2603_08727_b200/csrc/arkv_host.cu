@@ -96,7 +96,8 @@ arkv_status validate(const arkv_config* c) {
   if (c->quant_mode == ARKV_QUANT_FP8 && c->quant_bits != 8) return ARKV_ERR_CONFIG;
   if (c->max_positions <= 0 || c->max_prompt <= 0 || c->max_prompt > c->max_positions) return ARKV_ERR_CONFIG;
   if (c->alpha <= 0.0 || c->alpha > 1.0) return ARKV_ERR_CONFIG;
-  if (c->layout == ARKV_LAYOUT_FRAG && (c->quant_bits != 4 || c->head_dim % 32)) return ARKV_ERR_CONFIG;
+  const bool frag_ok = c->head_dim % 32 == 0 && (c->quant_bits == 4 || c->quant_mode == ARKV_QUANT_FP8);
+  if (c->layout == ARKV_LAYOUT_FRAG && !frag_ok) return ARKV_ERR_CONFIG;
   if (c->layout < 0 || c->layout > 2) return ARKV_ERR_CONFIG;
   if (c->decode_kernel < 0 || c->decode_kernel > 3) return ARKV_ERR_CONFIG;
   return ARKV_OK;
@@ -118,7 +119,8 @@ Sizes compute_sizes(const arkv_config& c) {
   g.mode = c.quant_mode;
   g.layout = c.layout;
   if (g.layout == ARKV_LAYOUT_AUTO)
-    g.layout = (c.quant_bits == 4 && c.head_dim % 32 == 0) ? ARKV_LAYOUT_FRAG : ARKV_LAYOUT_PLAIN;
+    g.layout = ((c.quant_bits == 4 || c.quant_mode == ARKV_QUANT_FP8) && c.head_dim % 32 == 0) ? ARKV_LAYOUT_FRAG
+                                                                                              : ARKV_LAYOUT_PLAIN;
   g.B = c.budget_tokens;
   g.cost_o = (int)cost_o(c);
   g.cost_q = (int)cost_q(c);

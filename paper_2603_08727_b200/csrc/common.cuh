@@ -112,8 +112,32 @@ __host__ __device__ inline int o_v_off(const Geom& g, int j, int x) {
   return 64 * g.d + lane_word(k, lane) * 4 + u * 2;
 }
 
+// FRAG, 8-bit codes (fp8 e4m3, NEXT-2): every code byte sits where the f16 mma.sync
+// fragment it converts into (one cvt.rn.f16x2.e4m3x2 per byte pair) needs it.
+//  K block (A operand of S = K q^T, M = tokens, K = dims): quad ((mt*d/32 + ks/2)*32 + lane),
+//    byte (ks&1)*8 + 2r + e holds token mt*16 + 8(r&1) + gg, dim 16ks + 8(r>>1) + 2t + e.
+//  V block (A operand of O^T = V^T P'^T, M = dims, K = tokens): quad (mtv*32 + lane),
+//    byte kc*8 + 2r + e holds dim 16mtv + 8(r&1) + gg, token 16kc + 8(r>>1) + 2t + e.
+//  (lane = 4gg + t; register r = row half + 2 * column half.)
+__host__ __device__ inline int f8_k_off(const Geom& g, int j, int x) {
+  const int mt = j >> 4, rh = (j >> 3) & 1, gg = j & 7;
+  const int ks = x >> 4, ch = (x >> 3) & 1, t = (x & 7) >> 1, e = x & 1;
+  return ((mt * (g.d >> 5) + (ks >> 1)) * 32 + 4 * gg + t) * 16 + (ks & 1) * 8 + (rh + 2 * ch) * 2 + e;
+}
+__host__ __device__ inline int f8_v_off(const Geom& g, int j, int x) {
+  const int mtv = x >> 4, rh = (x >> 3) & 1, gg = x & 7;
+  const int kc = j >> 4, ch = (j >> 3) & 1, t = (j & 7) >> 1, e = j & 1;
+  return 32 * g.d + (mtv * 32 + 4 * gg + t) * 16 + kc * 8 + (rh + 2 * ch) * 2 + e;
+}
+__host__ __device__ inline bool frag8(const Geom& g) { return g.layout == ARKV_LAYOUT_FRAG && g.bits == 8; }
+
 // Q tile codes: returns the byte offset of the byte holding the code and its bit shift.
 __host__ __device__ inline void q_k_loc(const Geom& g, int j, int x, int* byte, int* shift) {
+  if (frag8(g)) {
+    *byte = f8_k_off(g, j, x);
+    *shift = 0;
+    return;
+  }
   if (g.layout != ARKV_LAYOUT_FRAG) {
     int bit = x * g.bits;
     *byte = j * g.cost_q + (bit >> 3);
@@ -130,6 +154,11 @@ __host__ __device__ inline void q_k_loc(const Geom& g, int j, int x, int* byte, 
   *shift = (e & 1) * 4;
 }
 __host__ __device__ inline void q_v_loc(const Geom& g, int j, int x, int* byte, int* shift) {
+  if (frag8(g)) {
+    *byte = f8_v_off(g, j, x);
+    *shift = 0;
+    return;
+  }
   if (g.layout != ARKV_LAYOUT_FRAG) {
     int bit = x * g.bits;
     *byte = j * g.cost_q + (g.d * g.bits >> 3) + (bit >> 3);
@@ -150,6 +179,7 @@ __host__ __device__ inline void q_v_loc(const Geom& g, int j, int x, int* byte, 
 // which: 0 k_scale, 1 k_zero, 2 v_scale, 3 v_zero.
 __host__ __device__ inline int q_sc_off(const Geom& g, int j, int which, int grp) {
   if (g.layout != ARKV_LAYOUT_FRAG) return j * g.cost_q + 2 * (g.d * g.bits >> 3) + (which * g.ng + grp) * 4;
+  if (frag8(g)) return 64 * g.d + ((j * g.ng + grp) * 4 + which) * 4;
   // per row and group the four floats k_scale, k_zero, v_scale, v_zero are adjacent: one
   // 16-byte shared-memory load each in the decode kernel (conflict-free: rows 16 B apart)
   return 32 * g.d + ((j * g.ng + grp) * 4 + which) * 4;
@@ -165,6 +195,24 @@ __host__ __device__ inline bool q_code_slot(const Geom& g, int B, int s, int* j,
     *j = row;
     *isv = off >= cb;
     *x = (*isv ? off - cb : off) * per + s;
+    return true;
+  }
+  if (frag8(g)) {
+    if (B >= 64 * g.d) return false;
+    const bool v = B >= 32 * g.d;
+    const int bl = v ? B - 32 * g.d : B;
+    const int qd = bl >> 4, w = bl & 15, lane = qd & 31, gg = lane >> 2, t = lane & 3;
+    const int hk = w >> 3, r = (w & 7) >> 1, e = w & 1, rh = r & 1, ch = r >> 1;
+    if (!v) {
+      const int q = qd >> 5, nq = g.d >> 5, mt = q / nq, ks = (q % nq) * 2 + hk;
+      *j = mt * 16 + rh * 8 + gg;
+      *x = ks * 16 + ch * 8 + 2 * t + e;
+    } else {
+      const int mtv = qd >> 5;
+      *x = mtv * 16 + rh * 8 + gg;
+      *j = hk * 16 + ch * 8 + 2 * t + e;
+    }
+    *isv = v ? 1 : 0;
     return true;
   }
   if (B >= 32 * g.d) return false;

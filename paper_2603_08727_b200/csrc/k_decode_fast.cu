@@ -127,6 +127,13 @@ __device__ __forceinline__ void unpack8(uint32_t w, uint32_t (&x)[4]) {
   x[2] = hsub2_1024(lop3_mask_or(w8, 0x000F000Fu, 0x64006400u));
   x[3] = hsub2_1024(lop3_mask_or(w8, 0x00F000F0u, 0x64006400u));
 }
+// Two e4m3 codes (the low / high 16 bits of w) -> f16x2 (lower code -> lower half).
+__device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint32_t v16) {
+  const __half2_raw h = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(v16 & 0xFFFFu), __NV_E4M3);
+  return (uint32_t)h.x | ((uint32_t)h.y << 16);
+}
+__device__ __forceinline__ uint32_t e4m3x2_lo(uint32_t w) { return e4m3x2_to_f16x2(w); }
+__device__ __forceinline__ uint32_t e4m3x2_hi(uint32_t w) { return e4m3x2_to_f16x2(w >> 16); }
 // The same without the exact "- 1024": codes stay as f16 (1024 + c) / (1024 + 16c).  Used
 // for the PV contraction only, whose result tolerates the fp32 cancellation of the offset
 // (~1e-5 absolute on the output); the logits (QK), which decide token states through the
@@ -224,11 +231,29 @@ struct QFrag {
   uint32_t qb[8][2], qh[8][2];
   float qsum[2][NG];
 };
-template <int G, int NG>
+template <int G, int NG, bool F8>
 __device__ __forceinline__ void load_qfrag(const uint16_t* qp, int lane, QFrag<NG>& f) {
   const int gq = lane >> 2, tq = lane & 3;
   const int hq = gq;  // B operand column n = head gq
   const bool hv = hq < G;
+  if (F8) {
+    // fp8 Quantized tiles (FRAG, 8-bit): the standard f16 B fragment — k-step ks holds
+    // dims 16ks + 2t, +1 (b0) and 16ks + 2t + 8, +9 (b1); no zero point, no Σq
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int x0 = tq * 32 + 4 * c;
+      f.qb[c][0] = hv ? *(const uint32_t*)(qp + hq * D + x0) : 0u;
+      f.qb[c][1] = hv ? *(const uint32_t*)(qp + hq * D + x0 + 2) : 0u;
+      const int xb = 16 * c + 2 * tq;
+      f.qh[c][0] = hv ? pack_f16(bf16_to_f(qp[hq * D + xb]), bf16_to_f(qp[hq * D + xb + 1])) : 0u;
+      f.qh[c][1] = hv ? pack_f16(bf16_to_f(qp[hq * D + xb + 8]), bf16_to_f(qp[hq * D + xb + 9])) : 0u;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int gr = 0; gr < NG; ++gr) f.qsum[e][gr] = 0.f;
+    return;
+  }
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const int x0 = tq * 32 + 4 * c;  // Original tiles: dims t*(d/4)+4c+{0,1} / +{2,3}
@@ -291,7 +316,7 @@ __device__ __forceinline__ void acc_reset(Acc<NG>& s) {
 // Folds one staged 32-token tile into the warp's flash state.  tb: the tile in shared
 // memory; n_valid: rows in use; lrow: HH logit row base of this tile (a.logits + (u G)
 // row_stride + (isq ? cap_o : 0) + 32 tile) or nullptr outside the HH window.
-template <int G, int NG>
+template <int G, int NG, bool F8>
 __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_valid, float* lrow, int row_stride,
                                              const QFrag<NG>& f, Acc<NG>& s, float c2, bool sym, int lane,
                                              int src_lane) {
@@ -312,6 +337,41 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e) lg[mt][e] = acc[e] * c2;
+    }
+  } else if (F8) {
+    // fp8 e4m3 codes: one cvt.rn.f16x2.e4m3x2 per byte pair gives the f16 A fragment;
+    // logit = s_k · (q · e4m3(c)) (no zero point)
+    const float* sc = (const float*)(tb + 64 * D);  // [row][grp][k_scale, 0, v_scale, 0]
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      float acc[NG][4];
+#pragma unroll
+      for (int gr = 0; gr < NG; ++gr)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[gr][e] = 0.f;
+#pragma unroll
+      for (int kp = 0; kp < 4; ++kp) {
+        const uint4 r = lds128(tb + ((mt * 4 + kp) * 32 + lane) * 16);
+        const int gr0 = (32 * kp) / (D / NG), gr1 = (32 * kp + 16) / (D / NG);
+        mma_f16(acc[gr0], e4m3x2_lo(r.x), e4m3x2_hi(r.x), e4m3x2_lo(r.y), e4m3x2_hi(r.y), f.qh[2 * kp][0],
+                f.qh[2 * kp][1]);
+        mma_f16(acc[gr1], e4m3x2_lo(r.z), e4m3x2_hi(r.z), e4m3x2_lo(r.w), e4m3x2_hi(r.w), f.qh[2 * kp + 1][0],
+                f.qh[2 * kp + 1][1]);
+      }
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int j = mt * 16 + gq + 8 * hh;
+        float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+        for (int gr = 0; gr < NG; ++gr) {
+          const float ks = sc[(j * NG + gr) * 4];
+          l0 += ks * acc[gr][hh * 2 + 0];
+          l1 += ks * acc[gr][hh * 2 + 1];
+          zv[mt][hh][gr] = 0.f;
+        }
+        lg[mt][hh * 2 + 0] = l0 * c2;
+        lg[mt][hh * 2 + 1] = l1 * c2;
+      }
     }
   } else {
     const float* sc = (const float*)(tb + 32 * D);  // [row][grp][k_scale, k_zero, v_scale, v_zero]
@@ -450,6 +510,32 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
         if (G == 8) mma_bf16(s.o[mv], r.x, r.y, r.z, r.w, c01[kc], c23[kc]);
       }
     }
+  } else if (F8) {
+    // ---- PV on fp8 Quantized tiles: A = e4m3 V^T (converted), B = P' = p·s_v ----
+    const float* sc = (const float*)(tb + 64 * D);
+    uint32_t b01[NG][2], b23[NG][2], c01[NG][2], c23[NG][2];
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) {
+#pragma unroll
+      for (int gr = 0; gr < NG; ++gr) {
+        float pv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pv[e] = p[kc][e] * sc[((kc * 16 + gq + 8 * (e >> 1)) * NG + gr) * 4 + 2];
+        make_b<G, false>(pv, tq, b01[gr][kc], b23[gr][kc], c01[gr][kc], c23[gr][kc]);
+      }
+    }
+    const uint8_t* vb = tb + 32 * D;
+#pragma unroll
+    for (int mv = 0; mv < 8; ++mv) {
+      const uint4 r = lds128(vb + (mv * 32 + lane) * 16);
+      const int gr = (mv * 16) / (D / NG);
+      mma_f16(s.o[mv], e4m3x2_lo(r.x), e4m3x2_hi(r.x), e4m3x2_lo(r.y), e4m3x2_hi(r.y), b01[gr][0], b23[gr][0]);
+      if (G == 8)
+        mma_f16(s.o[mv], e4m3x2_lo(r.x), e4m3x2_hi(r.x), e4m3x2_lo(r.y), e4m3x2_hi(r.y), c01[gr][0], c23[gr][0]);
+      mma_f16(s.o[mv], e4m3x2_lo(r.z), e4m3x2_hi(r.z), e4m3x2_lo(r.w), e4m3x2_hi(r.w), b01[gr][1], b23[gr][1]);
+      if (G == 8)
+        mma_f16(s.o[mv], e4m3x2_lo(r.z), e4m3x2_hi(r.z), e4m3x2_lo(r.w), e4m3x2_hi(r.w), c01[gr][1], c23[gr][1]);
+    }
   } else {
     // ---- PV on Quantized tiles (f16 codes, P' = p·s_v / f) ----
     const float* sc = (const float*)(tb + 32 * D);
@@ -511,7 +597,7 @@ __device__ __forceinline__ void acc_reduce_rows(Acc<NG>& s) {
   }
 }
 
-template <int G, int NG, int C, int SPW>
+template <int G, int NG, int C, int SPW, bool F8>
 __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536) ? 2 : 1)
     decode_fast_kernel(DecodeArgs a) {
   constexpr int kConsumers = C;
@@ -647,7 +733,7 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536)
   } else {
     // ===================== consumers =====================
     QFrag<NG> qf;
-    load_qfrag<G, NG>(qp, lane, qf);
+    load_qfrag<G, NG, F8>(qp, lane, qf);
     Acc<NG> acc;
     acc_reset(acc);
     // lane holding the running max of the heads of this thread's O^T columns
@@ -666,7 +752,7 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536)
         const int tile = first + jt;
         const int n_valid = isq ? min(kTile, n_q - tile * kTile) : min(kTile, n_o - tile * kTile);
         float* lrow = accm ? a.logits + (int64_t)u * G * row_stride + (isq ? g.cap_o : 0) + tile * kTile : nullptr;
-        consume_tile<G, NG>(tb, isq, n_valid, lrow, row_stride, qf, acc, c2, sym, lane, src_lane);
+        consume_tile<G, NG, F8>(tb, isq, n_valid, lrow, row_stride, qf, acc, c2, sym, lane, src_lane);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[st]);
@@ -751,9 +837,9 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536)
   }
 }
 
-template <int G, int NG, int C, int SPW>
+template <int G, int NG, int C, int SPW, bool F8 = false>
 static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
-  auto kern = decode_fast_kernel<G, NG, C, SPW>;
+  auto kern = decode_fast_kernel<G, NG, C, SPW, F8>;
   const int smem = (int)sizeof(Smem<C, SPW>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   dim3 grid(a.n_splits, n_units_call);
@@ -767,6 +853,10 @@ static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
 // with ARKV_FAST_CFG=C,SPW (4,1 | 4,2 | 6,2 | 4,3 | 8,1).
 template <int G, int NG>
 static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+  if (a.g.mode == ARKV_QUANT_FP8) {
+    launch_cfg<G, NG, 4, 1, true>(a, n_units_call, s, ev0, ev1);
+    return;
+  }
   if (G == 4 && NG == 1) {
     const char* e = std::getenv("ARKV_FAST_CFG");
     const int cfg = e ? (e[0] - '0') * 10 + (e[2] - '0') : 41;
@@ -871,7 +961,7 @@ struct PSmem {
   int4 info[C][2];  // per stage, written by the producer: (ul, u, k, phase), (n_o, n_q, tiles_q, accm)
 };
 
-template <int G, int NG>
+template <int G, int NG, bool F8>
 __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
     decode_persist_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ PersistPlan plan) {
   constexpr int C = kPersistConsumers;
@@ -1006,20 +1096,20 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
     const int4 i0 = sm.info[st][0], i1 = sm.info[st][1];
     if (i0.x != cur) {
       if (cur >= 0) flush();
-      load_qfrag<G, NG>(punit_q(a, i0.x), lane, qf);
+      load_qfrag<G, NG, F8>(punit_q(a, i0.x), lane, qf);
       cur = i0.x;
       acc_reset(acc);
     }
     const int u = i0.y, k = i0.z;
     float* lbase = i1.w ? a.logits + (int64_t)u * G * row_stride : nullptr;
     if (i0.w == 0) {
-      consume_tile<G, NG>(sm.ring[st], false, min(kTile, i1.x - k * kTile), lbase ? lbase + k * kTile : nullptr,
+      consume_tile<G, NG, F8>(sm.ring[st], false, min(kTile, i1.x - k * kTile), lbase ? lbase + k * kTile : nullptr,
                           row_stride, qf, acc, c2, sym, lane, src_lane);
     } else {
       const int first = k * q_per, nt = min(q_per, i1.z - first);
       for (int jt = 0; jt < nt; ++jt) {
         const int tile = first + jt;
-        consume_tile<G, NG>(sm.ring[st] + (nt - 1 - jt) * g.tile_q, true, min(kTile, i1.y - tile * kTile),
+        consume_tile<G, NG, F8>(sm.ring[st] + (nt - 1 - jt) * g.tile_q, true, min(kTile, i1.y - tile * kTile),
                             lbase ? lbase + g.cap_o + tile * kTile : nullptr, row_stride, qf, acc, c2, sym, lane,
                             src_lane);
       }
@@ -1170,10 +1260,10 @@ __global__ void __launch_bounds__(G * D) decode_persist_combine(DecodeArgs a) {
   }
 }
 
-template <int G, int NG>
+template <int G, int NG, bool F8>
 static void launch_persist(const DecodeArgs& a, const PersistPlan& plan, int n_units_call, cudaStream_t s,
                            cudaEvent_t ev0, cudaEvent_t ev1) {
-  auto kern = decode_persist_kernel<G, NG>;
+  auto kern = decode_persist_kernel<G, NG, F8>;
   const int smem = (int)sizeof(PSmem<kPersistConsumers>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (ev0) cudaEventRecord(ev0, s);
@@ -1184,10 +1274,14 @@ static void launch_persist(const DecodeArgs& a, const PersistPlan& plan, int n_u
 template <int G>
 static int launch_persist_g(const DecodeArgs& a, const PersistPlan& plan, int n_units_call, cudaStream_t s,
                             cudaEvent_t ev0, cudaEvent_t ev1) {
+  const bool f8 = a.g.mode == ARKV_QUANT_FP8;
   switch (a.g.ng) {
-    case 1: launch_persist<G, 1>(a, plan, n_units_call, s, ev0, ev1); return 2;
-    case 2: launch_persist<G, 2>(a, plan, n_units_call, s, ev0, ev1); return 2;
-    case 4: launch_persist<G, 4>(a, plan, n_units_call, s, ev0, ev1); return 2;
+    case 1: f8 ? launch_persist<G, 1, true>(a, plan, n_units_call, s, ev0, ev1)
+               : launch_persist<G, 1, false>(a, plan, n_units_call, s, ev0, ev1); return 2;
+    case 2: f8 ? launch_persist<G, 2, true>(a, plan, n_units_call, s, ev0, ev1)
+               : launch_persist<G, 2, false>(a, plan, n_units_call, s, ev0, ev1); return 2;
+    case 4: f8 ? launch_persist<G, 4, true>(a, plan, n_units_call, s, ev0, ev1)
+               : launch_persist<G, 4, false>(a, plan, n_units_call, s, ev0, ev1); return 2;
     default: return -1;
   }
 }
@@ -1195,7 +1289,8 @@ static int launch_persist_g(const DecodeArgs& a, const PersistPlan& plan, int n_
 }  // namespace fast
 
 bool decode_fast_available(const Geom& g) {
-  return g.layout == ARKV_LAYOUT_FRAG && g.d == fast::D && g.bits == 4 && (g.ng == 1 || g.ng == 2 || g.ng == 4) &&
+  const bool fmt = g.bits == 4 || (g.bits == 8 && g.mode == ARKV_QUANT_FP8);
+  return g.layout == ARKV_LAYOUT_FRAG && g.d == fast::D && fmt && (g.ng == 1 || g.ng == 2 || g.ng == 4) &&
          (g.G == 1 || g.G == 2 || g.G == 4 || g.G == 8);
 }
 

@@ -109,12 +109,14 @@ def test_host_oq_score_equals_oracle(p):
 
 @pytest.mark.parametrize("d,bits,g,layout", [
     (16, 4, 16, 1), (16, 2, 16, 1), (16, 8, 8, 1), (32, 4, 32, 2), (64, 4, 32, 2), (128, 4, 128, 2),
-    (128, 4, 64, 2), (128, 4, 32, 2), (128, 2, 32, 1), (128, 8, 128, 1), (256, 4, 128, 2), (48, 4, 16, 1)])
+    (128, 4, 64, 2), (128, 4, 32, 2), (128, 2, 32, 1), (128, 8, 128, 1), (256, 4, 128, 2), (48, 4, 16, 1),
+    (128, 8, 128, 2), (128, 8, 16, 2), (64, 8, 32, 2), (256, 8, 64, 2)])
 def test_tile_layouts_are_bijections(d, bits, g, layout):
     """PLAIN and FRAG tile layouts: element -> byte maps are bijections covering the tile,
     and the code-slot inverse used by the tailor's packing pass inverts them."""
+    mode = A.QUANT_FP8 if (bits == 8 and layout == 2) else A.QUANT_ASYM   # 8-bit FRAG = fp8 codes
     c = A.make_config(1, 4, 2, d, window=8, budget_tokens=64, quant_bits=bits, group_size=g, layout=layout,
-                      max_positions=256)
+                      max_positions=256, quant_mode=mode)
     n = A.arkv_layout_check(c)
     assert n == 32 * d * 2 + 32 * d * 2 + 32 * 4 * (d // g)
 

@@ -131,6 +131,7 @@ MID = Shape(batch=1, n_layers=2, n_q_heads=8, n_kv_heads=2, head_dim=128, prompt
     (2, 4, 64, "sym"),
     (1, 8, 128, "fp8"),    # NEXT-2: e4m3 codes, per-token scale
     (1, 8, 32, "fp8"),
+    (2, 8, 128, "fp8"),    # fp8 in the fragment-native layout (tensor-core kernel)
 ])
 def test_mid_config(layout, bits, g, mode):
     """L=2, H_q=8, H_kv=2, d=128, P=2048, B=512: prefill tailor + decode tailors."""
@@ -182,6 +183,15 @@ def test_persistent_matches_split_states():
     for e2, e3 in zip(res[0][1], res[1][1]):
         for key in ("state", "q_k", "k_scale", "o_k", "o_v"):
             np.testing.assert_array_equal(e2[key], e3[key])
+
+
+@pytest.mark.parametrize("kernel,g", [(1, 128), (2, 128), (3, 128), (2, 32), (3, 64)])
+def test_fp8_frag_kernels(kernel, g):
+    """fp8 e4m3 Q tokens (NEXT-2) in the FRAG layout: generic, split-K and persistent
+    decode kernels (cvt.rn.f16x2.e4m3x2 fragments) against the oracle."""
+    r = run_parity(MID, budget=512, steps=64, seed=8, rho=[[0.8, 0.3]], layout=2, bits=8, g=g, mode="fp8",
+                   decode_kernel=kernel, check_every=16)
+    assert r["tailors"] >= 2 * 2 * 2
 
 
 def test_batch_and_spare_waves():
