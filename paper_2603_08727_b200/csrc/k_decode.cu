@@ -368,6 +368,8 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
     a.interleave = e2 ? std::atoi(e2) : 0;        // measured: interleaving O/Q items is slower
     const char* e3 = std::getenv("ARKV_FUSE_COMBINE");
     a.fuse_combine = e3 ? std::atoi(e3) : 0;      // measured: the separate combine kernel is faster
+    const char* e5 = std::getenv("ARKV_PREFETCH");
+    a.prefetch = e5 ? std::atoi(e5) : 0;
     const char* e4 = std::getenv("ARKV_ITEM_ORDER");
     a.item_order = e4 ? std::atoi(e4) : 1;  // measured: alternating O-first / Q-first CTAs -1.2 %
   }

@@ -80,6 +80,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Bulk prefetch of [src, src + bytes) into L2 (no completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint4 lds128(const void* p) {
   uint4 r;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
@@ -680,14 +684,32 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536)
     if (lane == 0) {
       // items in order (measured: polling stages out of order and busy-waiting costs the
       // co-scheduled consumer warp issue slots; try_wait suspends in hardware)
-      for (int i = 0; i < n_work; ++i) {
-        const int st = stage_of(i);
-        if (i >= kStages) mbar_wait(&sm.empty[st], (phase_of(i) - 1) & 1);
+      auto item_src = [&](int i, const uint8_t*& src, uint32_t& bytes) {
         bool isq;
         int first, ntiles;
         item_of(i, isq, first, ntiles);
-        const uint8_t* src = isq ? q_tile_ptr(slot, g, first + ntiles - 1) : o_tile_ptr(slot, g, first);
-        const uint32_t bytes = isq ? (uint32_t)(ntiles * g.tile_q) : (uint32_t)g.tile_o;
+        src = isq ? q_tile_ptr(slot, g, first + ntiles - 1) : o_tile_ptr(slot, g, first);
+        bytes = isq ? (uint32_t)(ntiles * g.tile_q) : (uint32_t)g.tile_o;
+      };
+      const int ahead = a.prefetch;  // items requested into L2 ahead of the ring (0: off)
+      for (int i = 0; i < min(ahead, n_work); ++i) {
+        const uint8_t* src;
+        uint32_t bytes;
+        item_src(kStages + i, src, bytes);
+        if (kStages + i < n_work) bulk_prefetch_l2(src, bytes);
+      }
+      for (int i = 0; i < n_work; ++i) {
+        const int st = stage_of(i);
+        if (ahead > 0 && i + kStages + ahead < n_work) {
+          const uint8_t* psrc;
+          uint32_t pbytes;
+          item_src(i + kStages + ahead, psrc, pbytes);
+          bulk_prefetch_l2(psrc, pbytes);
+        }
+        if (i >= kStages) mbar_wait(&sm.empty[st], (phase_of(i) - 1) & 1);
+        const uint8_t* src;
+        uint32_t bytes;
+        item_src(i, src, bytes);
         mbar_expect_tx(&sm.full[st], bytes);
         bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
       }

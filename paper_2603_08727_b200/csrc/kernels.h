@@ -58,6 +58,7 @@ struct DecodeArgs {
   int q_group;        // fast kernel: Quantized tiles per bulk copy (0 = as many as fit a stage)
   int interleave;     // fast kernel: interleave Original and Quantized work items
   int fuse_combine;   // fast kernel: the last split CTA of a unit merges the partials
+  int prefetch;       // fast kernel: items prefetched into L2 ahead of the shared-memory ring
   int item_order;     // fast kernel: 0 Original tiles first; 1 Quantized groups first on odd
                       // (split + unit) CTAs; 2 Quantized groups first everywhere
   void* out;
