@@ -39,6 +39,8 @@ class Cfg:
     budget_tokens: int = 512         # B in bf16-token equivalents per (seq, layer, kv head) (R10, R11)
     quant_bits: int = 4              # R23
     group_size: int = 0              # 0 -> head_dim ("per-token scale")
+    state_sharing: str = "head"      # "head": one state set per KV head (R20) | "layer": SPEC's
+                                     # S:231 score averaged across the layer's groups (NEXT-3)
     quant_mode: str = "asym"         # "asym" (scale, zero=min) | "sym" |
                                      # "fp8" (e4m3 codes, per-group scale: P:333; NEXT-2)
     alpha: float = 0.75
@@ -74,6 +76,8 @@ def validate(cfg: Cfg) -> None:
         raise ValueError("head_dim*bits must be a whole number of bytes")
     if cfg.budget_tokens <= 2 * cfg.window:
         raise ValueError("budget must exceed 2W (R14)")
+    if cfg.state_sharing not in ("head", "layer"):
+        raise ValueError("state_sharing")
     if cfg.quant_mode not in ("asym", "sym", "fp8"):
         raise ValueError("quant_mode")
     if cfg.quant_mode == "fp8" and cfg.quant_bits != 8:
@@ -501,28 +505,42 @@ class UnitCache:
         pos = np.concatenate([self.o_pos, self.q_pos])
         return pos, np.vstack([self.o_k, qk]), np.vstack([self.o_v, qv])
 
-    def tailor(self, rho: float, rows, tailor_pos: int):
-        """Eq. 10 tailor (P:232-251; Alg. 1 P:281-292) with the D6 transitions:
-        O->Q quantize, Q->O promote (R24), Q->Q keep codes (R25), ->E drop.
-        rows: list of (key positions [n], probs [r][n]) — the Eq. 2 window rows
-        (R19); every eligible token must appear in every row.  Parity unpinned: which
-        queries form the decode-time window (R19) is this design's reading.""" 
-        cfg = self.cfg
-        W = cfg.window
-        K = self.n_o + self.n_q
-        n_oe, n_q = tailor_counts(K, rho, cfg)
-        # window = the W highest positions, all Original (A13)
+    def eligible(self):
+        """(eligible positions ascending, window positions): the window is the W highest
+        positions, all Original (A13)."""
+        W = self.cfg.window
         allpos = np.concatenate([self.o_pos, self.q_pos])
         win = set(np.sort(allpos)[-W:].tolist())
         assert all(p in set(self.o_pos.tolist()) for p in win), "window must be Original"
         elig = np.array(sorted(p for p in allpos.tolist() if p not in win), dtype=np.int64)
+        return elig, win
+
+    def scores(self, rows) -> np.ndarray:
+        """Eq. 9 scores of the eligible tokens (ascending positions) from the Eq. 2 window
+        rows: list of (key positions [n], probs [r][n]) (R19)."""
+        elig, _ = self.eligible()
         blocks = []
         for kpos, pr in rows:
             col = {int(p): i for i, p in enumerate(np.asarray(kpos).tolist())}
             missing = [p for p in elig.tolist() if p not in col]
             assert not missing, "eligible token without window samples"
             blocks.append(np.asarray(pr, dtype=np.float64)[:, [col[int(p)] for p in elig]])
-        S = hh_scores(np.concatenate(blocks, axis=0), cfg.gamma)
+        return hh_scores(np.concatenate(blocks, axis=0), self.cfg.gamma)
+
+    def tailor(self, rho: float, rows, tailor_pos: int, scores=None):
+        """Eq. 10 tailor (P:232-251; Alg. 1 P:281-292) with the D6 transitions:
+        O->Q quantize, Q->O promote (R24), Q->Q keep codes (R25), ->E drop.
+        rows: list of (key positions [n], probs [r][n]) — the Eq. 2 window rows
+        (R19); every eligible token must appear in every row.  Parity unpinned: which
+        queries form the decode-time window (R19) is this design's reading.
+        scores: precomputed eligible-token scores (layer-shared states, NEXT-3)."""
+        cfg = self.cfg
+        W = cfg.window
+        K = self.n_o + self.n_q
+        n_oe, n_q = tailor_counts(K, rho, cfg)
+        elig, win = self.eligible()
+        S = self.scores(rows) if scores is None else np.asarray(scores, dtype=np.float64)
+        assert len(S) == len(elig)
         st = plan_states(S, elig, n_oe, n_q)
         # score margin at the two rank thresholds (exact ties are resolved by position
         # identically on both sides; near-ties would make fp32 vs fp64 rankings differ)
@@ -628,9 +646,11 @@ class OracleARKV:
         self.rho = rho
         for b in range(Bn):
             for l in range(L):
+                rows = {}
                 for kvh in range(Hkv):
                     u = UnitCache(cfg)
                     u.ingest(k[b, l, kvh], v[b, l, kvh])
+                    self.units[(b, l, kvh)] = u
                     if prefill_needs_tailor(P, cfg):
                         if at is None:
                             at = {}
@@ -638,10 +658,24 @@ class OracleARKV:
                         if a is None:
                             a = windowed_attention(q_win[b, l], k[b, l], cfg)
                             at[(b, l)] = a
-                        grp = a[kvh * G:(kvh + 1) * G].reshape(G * W, P - W)
-                        u.tailor(rho[b, l], [(np.arange(P - W), grp)], P)
-                    self.units[(b, l, kvh)] = u
+                        rows[kvh] = [(np.arange(P - W), a[kvh * G:(kvh + 1) * G].reshape(G * W, P - W))]
+                if rows:
+                    self._tailor_layer(b, l, rows, P)
         return stats, oq, rho
+
+    def _tailor_layer(self, b, l, rows, pos):
+        """Tailor of every KV head of (b, l): independent selections (R20), or one
+        selection from the score averaged across the groups (NEXT-3)."""
+        units = [self.units[(b, l, kvh)] for kvh in range(self.cfg.n_kv_heads)]
+        if self.cfg.state_sharing == "head":
+            for kvh, u in enumerate(units):
+                u.tailor(self.rho[b, l], rows[kvh], pos)
+            return
+        elig = [u.eligible()[0] for u in units]
+        assert all(np.array_equal(e, elig[0]) for e in elig), "layer-shared units hold the same tokens"
+        S = np.mean([u.scores(rows[kvh]) for kvh, u in enumerate(units)], axis=0)
+        for kvh, u in enumerate(units):
+            u.tailor(self.rho[b, l], rows[kvh], pos, scores=S)
 
     def decode_step(self, q, k, v, layer0: int = 0):
         """q [B][n][H_q][d], k, v [B][n][H_kv][d] for layers layer0..layer0+n-1.
@@ -653,6 +687,7 @@ class OracleARKV:
         for b in range(Bn):
             for li in range(n):
                 l = layer0 + li
+                rows = {}
                 for kvh in range(cfg.n_kv_heads):
                     u = self.units[(b, l, kvh)]
                     t = u.n_pos
@@ -662,7 +697,13 @@ class OracleARKV:
                         assert len(hist) == W and [h[0] for h in hist] == list(range(t - W, t)), \
                             "tailor window must be the last W queries"
                         assert hist[0][0] >= u.last_tailor_pos, "window rows must postdate the previous tailor (R14)"
-                        u.tailor(self.rho[b, l], [(h[1], h[2]) for h in hist], t)
+                        rows[kvh] = [(h[1], h[2]) for h in hist]
+                if rows:
+                    assert len(rows) == cfg.n_kv_heads   # counts are identical across KV heads (R15)
+                    self._tailor_layer(b, l, rows, t)
+                for kvh in range(cfg.n_kv_heads):
+                    u = self.units[(b, l, kvh)]
+                    t = u.n_pos - 1
                     pos, keys, vals = u.keys_values()
                     o, p = attention(q[b, li, kvh * G:(kvh + 1) * G], keys, vals, cfg.sm_scale)
                     out[b, li, kvh * G:(kvh + 1) * G] = o
