@@ -82,7 +82,9 @@ typedef struct arkv_config {
   double gamma;          /* HH variance weight 263.81 */
   double stat_eps;       /* clamp of H, V, K (R6), 1e-30 */
   float sm_scale;        /* softmax scale, 0 -> 1/sqrt(d) (R27) */
-  float pad_;
+  int32_t state_sharing; /* 0: one token-state set per KV head (R20); 1: one per layer, from the
+                            Eq. 9 score averaged across the layer's KV heads (NEXT-3;
+                            all KV heads of a layer must live in this cache) */
 } arkv_config;
 
 typedef struct arkv_cache arkv_cache; /* opaque, host-side; owned by the library */

@@ -31,6 +31,7 @@ struct arkv_cache {
   float* logits = nullptr;
   int8_t* st_scratch = nullptr;
   int32_t* src_scratch = nullptr;
+  float* sscore = nullptr;
   float* pf_partials = nullptr;
   float2* acc_pf = nullptr;
   double* oq_tmp = nullptr;
@@ -70,7 +71,7 @@ struct Sizes {
   int n_spare, jobs_per_wave, jobs_scratch, max_splits, n_chunks1;
   int64_t arena, ws;
   int64_t off_meta, off_desc, off_err;
-  int64_t w_partials, w_logits, w_st, w_src, w_pfp, w_accpf, w_oq, w_colsum, w_mstat, w_counters, w_plan, w_pparts;
+  int64_t w_partials, w_logits, w_st, w_sscore, w_src, w_pfp, w_accpf, w_oq, w_colsum, w_mstat, w_counters, w_plan, w_pparts;
 };
 
 int64_t cost_o(const arkv_config& c) { return 4LL * c.head_dim; }
@@ -100,6 +101,9 @@ arkv_status validate(const arkv_config* c) {
   if (c->layout == ARKV_LAYOUT_FRAG && !frag_ok) return ARKV_ERR_CONFIG;
   if (c->layout < 0 || c->layout > 2) return ARKV_ERR_CONFIG;
   if (c->decode_kernel < 0 || c->decode_kernel > 3) return ARKV_ERR_CONFIG;
+  if (c->state_sharing != 0 && c->state_sharing != 1) return ARKV_ERR_CONFIG;
+  // layer-shared tailors run a layer's KV heads in one wave (one spare slot each)
+  if (c->state_sharing == 1 && c->n_spare_slots > 0 && c->n_spare_slots < c->n_kv_heads) return ARKV_ERR_CONFIG;
   return ARKV_OK;
 }
 
@@ -117,6 +121,7 @@ Sizes compute_sizes(const arkv_config& c) {
   g.g = c.group_size ? c.group_size : c.head_dim;
   g.ng = g.d / g.g;
   g.mode = c.quant_mode;
+  g.share = c.state_sharing;
   g.layout = c.layout;
   if (g.layout == ARKV_LAYOUT_AUTO)
     g.layout = ((c.quant_bits == 4 || c.quant_mode == ARKV_QUANT_FP8) && c.head_dim % 32 == 0) ? ARKV_LAYOUT_FRAG
@@ -158,6 +163,8 @@ Sizes compute_sizes(const arkv_config& c) {
   s.w_st = w;
   const int64_t st_stride = std::max<int64_t>(g.max_pos, g.cap_o) + g.cap_q;
   w = round_up(w + (int64_t)s.jobs_scratch * st_stride, 256);
+  s.w_sscore = w;  // layer-shared scores of the eligible rows, per job
+  w = round_up(w + (c.state_sharing ? (int64_t)s.jobs_scratch * st_stride * 4 : 0), 256);
   s.w_src = w;
   w = round_up(w + (int64_t)s.jobs_scratch * (g.cap_o + g.cap_q) * 4, 256);
   s.w_pfp = w;
@@ -410,6 +417,7 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   c->logits = (float*)(w + s.w_logits);
   c->st_scratch = (int8_t*)(w + s.w_st);
   c->src_scratch = (int32_t*)(w + s.w_src);
+  c->sscore = (float*)(w + s.w_sscore);
   c->pf_partials = (float*)(w + s.w_pfp);
   c->acc_pf = (float2*)(w + s.w_accpf);
   c->oq_tmp = (double*)(w + s.w_oq);
@@ -508,7 +516,8 @@ int32_t arkv_cache_info(const arkv_cache* c, int32_t what) {
 static arkv_status run_jobs(arkv_cache* c, std::vector<TailorJob>& jobs, const uint16_t* pk, const uint16_t* pv, int P,
                             cudaStream_t s) {
   const Geom& g = c->g;
-  const int wave = pk ? c->jobs_per_prefill_wave : c->jobs_per_wave;  // prefill jobs need no spare slot
+  int wave = pk ? c->jobs_per_prefill_wave : c->jobs_per_wave;  // prefill jobs need no spare slot
+  if (g.share) wave -= wave % g.Hkv;  // a layer's KV heads select together (jobs come in (b, l, kvh) order)
   size_t i = 0;
   while (i < jobs.size()) {
     const int n = (int)std::min<size_t>(jobs.size() - i, (size_t)wave);
@@ -530,7 +539,7 @@ static arkv_status run_jobs(arkv_cache* c, std::vector<TailorJob>& jobs, const u
       if (no > g.cap_o + 0 || jb.n_q_new > g.cap_q) return ARKV_ERR_CAPACITY;
     }
     int nl = launch_tailor(g, tj, n, max_tiles, c->slots, c->meta, c->desc, pk, pv, P, c->acc_pf, c->st_scratch,
-                           c->src_scratch, c->err, s);
+                           c->src_scratch, c->sscore, c->err, s);
     if (nl < 0) return ARKV_ERR_CONFIG;
     c->launches += nl;
     debug_sync(s, "tailor");

@@ -42,6 +42,7 @@ struct Geom {
   int64_t slot_bytes;             // bytes per slot (two-stack)
   int64_t meta_bytes;             // per-slot metadata: pos_o, pos_q, acc_o, acc_q
   float sm_scale, gamma;
+  int32_t share;                  // 1: layer-shared token states (NEXT-3)
 };
 
 struct __align__(32) UnitDesc {

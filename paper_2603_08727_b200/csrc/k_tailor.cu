@@ -48,24 +48,20 @@ struct RowView {
   }
 };
 
-__global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs jobs, uint8_t* meta,
-                                                             const float2* __restrict__ acc_pf,
-                                                             int8_t* __restrict__ st_scratch, int st_stride) {
-  __shared__ uint32_t hist[2][256];
-  __shared__ uint64_t sh_prefix[2];
-  __shared__ uint32_t sh_rem[2];
-  griddep_wait();
-  const TailorJob jb = jobs.j[blockIdx.x];
-  int8_t* st = st_scratch + (int64_t)blockIdx.x * st_stride;  // [old O rows | old Q rows]
-  const int n_elig_o = jb.n_o_old - jb.n_win_old;
-  const int n_e = n_elig_o + jb.n_q_old;
-  const int q_off = st_stride - g.cap_q;
-
-  // window rows are always Original (A13); identity jobs keep every row Original
-  for (int i = threadIdx.x; i < jb.n_o_old; i += blockDim.x)
-    if (i >= n_elig_o || jb.identity) st[i] = 1;
-  if (jb.identity) return;
-
+// Score -> 64-bit composite key (S desc, position asc; R22).
+__device__ __forceinline__ uint64_t score_key(float S, int pos) {
+  uint32_t b = __float_as_uint(S);
+  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);  // order-preserving map of fp32
+  if (S == 0.f) b = 0x80000000u;                    // -0 == +0
+  return ((uint64_t)b << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)pos);
+}
+__device__ __forceinline__ float hh_score(float2 acc, float invN, float gamma) {
+  float mu = __fmul_rn(acc.x, invN);
+  float var = fmaxf(__fsub_rn(__fmul_rn(acc.y, invN), __fmul_rn(mu, mu)), 0.f);
+  return __fadd_rn(mu, __fmul_rn(gamma, var));
+}
+__device__ __forceinline__ RowView make_rowview(const Geom& g, const TailorJob& jb, uint8_t* meta,
+                                               const float2* acc_pf) {
   RowView rv;
   if (jb.old_slot < 0) {
     rv.acc_o = acc_pf + (int64_t)jb.unit * g.max_pos;
@@ -81,10 +77,62 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
     rv.pos_q = sm.pos_q;
     rv.prefill = false;
   }
-  rv.n_elig_o = n_elig_o;
+  rv.n_elig_o = jb.n_o_old - jb.n_win_old;
   rv.n_q = jb.n_q_old;
+  return rv;
+}
+
+__global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs jobs, uint8_t* meta,
+                                                             const float2* __restrict__ acc_pf,
+                                                             int8_t* __restrict__ st_scratch, int st_stride,
+                                                             float* __restrict__ sscore, int32_t* err) {
+  __shared__ uint32_t hist[2][256];
+  __shared__ uint64_t sh_prefix[2];
+  __shared__ uint32_t sh_rem[2];
+  griddep_wait();
+  const TailorJob jb = jobs.j[blockIdx.x];
+  int8_t* st = st_scratch + (int64_t)blockIdx.x * st_stride;  // [old O rows | old Q rows]
+  const int n_elig_o = jb.n_o_old - jb.n_win_old;
+  const int n_e = n_elig_o + jb.n_q_old;
+  const int q_off = st_stride - g.cap_q;
+
+  // window rows are always Original (A13); identity jobs keep every row Original
+  for (int i = threadIdx.x; i < jb.n_o_old; i += blockDim.x)
+    if (i >= n_elig_o || jb.identity) st[i] = 1;
+  if (jb.identity) return;
+
+  const RowView rv = make_rowview(g, jb, meta, acc_pf);
   const float invN = 1.0f / (float)(g.G * g.W);
   const float gamma = g.gamma;
+  // layer-shared states (NEXT-3): the score is the mean over the layer's KV
+  // heads, whose jobs are consecutive in this wave (run_jobs aligns waves to layers) and
+  // whose rows hold the same positions in the same order
+  float* ss = g.share ? sscore + (int64_t)blockIdx.x * st_stride : nullptr;
+  if (g.share) {
+    const int k0 = blockIdx.x - (blockIdx.x % g.Hkv);
+    for (int i = threadIdx.x; i < n_e; i += blockDim.x) {
+      float2 a;
+      int p;
+      rv.get(i, a, p);
+      float sum = 0.f;
+      for (int h = 0; h < g.Hkv; ++h) {
+        const RowView sv = make_rowview(g, jobs.j[k0 + h], meta, acc_pf);
+        float2 ah;
+        int ph;
+        sv.get(i, ah, ph);
+        if (ph != p) atomicOr(err, kErrIntegrity);
+        sum = __fadd_rn(sum, hh_score(ah, invN, gamma));
+      }
+      ss[i] = __fdiv_rn(sum, (float)g.Hkv);
+    }
+    __syncthreads();
+  }
+  auto key_of = [&](int i) -> uint64_t {
+    float2 a;
+    int p;
+    rv.get(i, a, p);
+    return g.share ? score_key(__ldcg(ss + i), p) : hh_key(a, p, invN, gamma);
+  };
 
   const uint32_t kk[2] = {(uint32_t)jb.n_oe, (uint32_t)(jb.n_oe + jb.n_q_new)};
   if (threadIdx.x < 2) {
@@ -108,10 +156,7 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
     __syncthreads();
     const int sh = pass * 8;
     for (int i = threadIdx.x; i < n_e; i += blockDim.x) {
-      float2 a;
-      int p;
-      rv.get(i, a, p);
-      const uint64_t key = hh_key(a, p, invN, gamma);
+      const uint64_t key = key_of(i);
       const uint32_t dg = (uint32_t)(key >> sh) & 0xFFu;
       if (!d0 && (key & m0) == p0) atomicAdd(&hist[0][dg], 1u);
       if (!d1 && (key & m1) == p1) atomicAdd(&hist[1][dg], 1u);
@@ -149,10 +194,7 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
   const uint64_t T1 = kk[0] == 0 ? ~0ull : sh_prefix[0];
   const uint64_t T2 = kk[1] == 0 ? ~0ull : sh_prefix[1];
   for (int i = threadIdx.x; i < n_e; i += blockDim.x) {
-    float2 a;
-    int p;
-    rv.get(i, a, p);
-    uint64_t key = hh_key(a, p, invN, gamma);
+    const uint64_t key = key_of(i);
     int8_t s = key >= T1 ? 1 : (key >= T2 ? 2 : 3);
     if (i < n_elig_o)
       st[i] = s;
@@ -728,10 +770,11 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
 
 int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_tiles, uint8_t* slots, uint8_t* meta,
                   UnitDesc* desc, const uint16_t* pk, const uint16_t* pv, int P, const float2* acc_pf,
-                  int8_t* st_scratch, int32_t* src_scratch, int32_t* err, cudaStream_t s) {
+                  int8_t* st_scratch, int32_t* src_scratch, float* sscore, int32_t* err, cudaStream_t s) {
   const int st_stride = max(g.max_pos, g.cap_o) + g.cap_q;
   const int src_stride = g.cap_o + g.cap_q;
-  launch_pdl(tailor_select_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, meta, acc_pf, st_scratch, st_stride);
+  launch_pdl(tailor_select_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, meta, acc_pf, st_scratch, st_stride,
+             sscore, err);
   launch_pdl(tailor_scan_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, desc, (const int8_t*)st_scratch, st_stride,
              src_scratch, src_stride, err);
   dim3 grid(max_tiles, n_jobs);

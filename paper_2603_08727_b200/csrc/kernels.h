@@ -40,7 +40,7 @@ int launch_prefill_finish(const Geom& g, const double* colsum, int P, double* st
 // Tailor of a wave of jobs (D4-D6).
 int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_tiles, uint8_t* slots, uint8_t* meta,
                   UnitDesc* desc, const uint16_t* pk, const uint16_t* pv, int P, const float2* acc_pf,
-                  int8_t* st_scratch, int32_t* src_scratch, int32_t* err, cudaStream_t s);
+                  int8_t* st_scratch, int32_t* src_scratch, float* sscore, int32_t* err, cudaStream_t s);
 
 struct DecodeArgs {
   Geom g;

@@ -55,6 +55,12 @@ def test_config_validation():
         A.arkv_cache_bytes(c)
     a, w = A.arkv_cache_bytes(A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, max_positions=128))
     assert a > 0 and w > 0
+    c = A.make_config(1, 8, 4, 16, window=8, budget_tokens=32, state_sharing=1, n_spare_slots=2)  # < H_kv spares
+    with pytest.raises(A.ArkvError):
+        A.arkv_cache_bytes(c)
+    c = A.make_config(1, 8, 4, 16, window=8, budget_tokens=32, state_sharing=2)
+    with pytest.raises(A.ArkvError):
+        A.arkv_cache_bytes(c)
     a8, _ = A.arkv_cache_bytes(A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, max_positions=128,
                                              quant_bits=8, quant_mode=A.QUANT_FP8))
     assert a8 > 0

@@ -42,17 +42,18 @@ def _bf16_bits_to_f64(u16):
 
 
 def make_pair(sh: Shape, budget, bits=4, g=0, mode="asym", layout=0, steps=64, decode_kernel=0, max_splits=0,
-              n_spare=0):
+              n_spare=0, sharing="head"):
     from paper_2603_08727_b200 import arkv as A
     cfg = A.make_config(sh.n_layers, sh.n_q_heads, sh.n_kv_heads, sh.head_dim, batch=sh.batch, window=sh.window,
                         budget_tokens=budget, quant_bits=bits, group_size=g,
                         quant_mode={"asym": A.QUANT_ASYM, "sym": A.QUANT_SYM, "fp8": A.QUANT_FP8}[mode],
                         max_positions=sh.prompt_len + steps + 1, max_prompt=sh.prompt_len, layout=layout,
-                        decode_kernel=decode_kernel, max_splits=max_splits, n_spare_slots=n_spare)
+                        decode_kernel=decode_kernel, max_splits=max_splits, n_spare_slots=n_spare,
+                        state_sharing=1 if sharing == "layer" else 0)
     gpu = A.ArkvCache(cfg, "cuda")
     ocfg = O.Cfg(n_layers=sh.n_layers, n_q_heads=sh.n_q_heads, n_kv_heads=sh.n_kv_heads, head_dim=sh.head_dim,
                  batch=sh.batch, window=sh.window, budget_tokens=budget, quant_bits=bits, group_size=g or sh.head_dim,
-                 quant_mode=mode)
+                 quant_mode=mode, state_sharing=sharing)
     return gpu, O.OracleARKV(ocfg), ocfg
 
 
@@ -192,6 +193,22 @@ def test_fp8_frag_kernels(kernel, g):
     r = run_parity(MID, budget=512, steps=64, seed=8, rho=[[0.8, 0.3]], layout=2, bits=8, g=g, mode="fp8",
                    decode_kernel=kernel, check_every=16)
     assert r["tailors"] >= 2 * 2 * 2
+
+
+@pytest.mark.parametrize("hkv,kernel", [(2, 0), (4, 0), (4, 3)])
+def test_layer_shared_states(hkv, kernel):
+    """NEXT-3: one token-state set per layer from the score averaged across its KV heads
+     — prefill-end and decode tailors against the oracle."""
+    sh = Shape(batch=2, n_layers=2, n_q_heads=4 * hkv, n_kv_heads=hkv, head_dim=128, prompt_len=1024, window=32)
+    r = run_parity(sh, budget=256, steps=48, seed=13, rho=[[0.7, 0.3], [0.5, 1.0]], layout=2, bits=4, g=128,
+                   decode_kernel=kernel, sharing="layer", check_every=16)
+    assert r["tailors"] >= 2 * 2 * hkv
+    gpu = r["gpu"]
+    for b in range(2):
+        for l in range(2):
+            st = [gpu.arkv_export_unit(b, l, h)["state"] for h in range(hkv)]
+            for h in range(1, hkv):
+                np.testing.assert_array_equal(st[h], st[0])
 
 
 def test_batch_and_spare_waves():
