@@ -191,6 +191,25 @@ arkv_status arkv_schedule(const arkv_config* cfg, int32_t prompt_len, double rho
    the tailor's packing pass inverts the forward map.  ARKV_ERR_DEVICE on a violation. */
 arkv_status arkv_layout_check(const arkv_config* cfg, int64_t* n_checked);
 
+/* Layer-shared token states across KV-head shards (state_sharing = 1, NEXT-3; collective
+   C3 of DESIGN.md §8).  The group-averaged tailor score needs every KV head of
+   the layer; when a sequence's heads are split over processes:
+   1. arkv_tailor_scores (async on stream): for each (sequence, layer) whose tailor the NEXT
+      call runs — arkv_prefill_finish after arkv_prefill_begin (every (b, l) when the prompt
+      needs the prefill-end tailor), else arkv_decode_step(layer0, n_layers) — writes row
+      r = d_scores[r * stride + i], the fp32 sum over this cache's KV heads of the Eq. 9
+      score of eligible row i, in (b, l) order; *n_rows = the rows written (0: no tailor).
+      ARKV_ERR_CAPACITY when max_rows or stride (>= eligible rows) is too small.
+   2. The caller sums the buffers across the shards (NCCL all-reduce, in place).
+   3. arkv_set_tailor_scores(cache, d_sum, stride, total_kv_heads): the next
+      arkv_decode_step / arkv_prefill_finish uses sum / total_kv_heads as the score of its
+      tailors, then forgets the pointer (the buffer must stay valid until that call's work
+      has run on its stream).
+   Without step 3 the score averages this cache's KV heads only. */
+arkv_status arkv_tailor_scores(arkv_cache* cache, int32_t layer0, int32_t n_layers, float* d_scores, int64_t stride,
+                               int32_t max_rows, int32_t* n_rows, void* stream);
+arkv_status arkv_set_tailor_scores(arkv_cache* cache, const float* d_scores, int64_t stride, int32_t total_kv_heads);
+
 /* Host only.  Builds the persistent decode kernel's work plan (decode_kernel = 3;
    DESIGN.md §6) for n_units units with the given Original / Quantized row counts and at
    most max_ctas CTAs, then replays one step on the host — the producer's unit-merged item

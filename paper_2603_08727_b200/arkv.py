@@ -48,6 +48,7 @@ EXPORTED = [
     "arkv_check", "arkv_schedule", "arkv_oq_score", "arkv_launch_count", "arkv_version",
     "arkv_status_string", "arkv_cache_info", "arkv_prefill_begin", "arkv_prefill_finish",
     "arkv_profile", "arkv_profile_read", "arkv_layout_check", "arkv_persist_plan_check",
+    "arkv_tailor_scores", "arkv_set_tailor_scores",
 ]
 
 _lib = None
@@ -74,6 +75,8 @@ def lib() -> ctypes.CDLL:
         L.arkv_oq_score.argtypes = [P(ArkvConfig), dbl, dbl, dbl, P(dbl), P(dbl)]
         L.arkv_layout_check.argtypes = [P(ArkvConfig), P(ctypes.c_int64)]
         L.arkv_persist_plan_check.argtypes = [P(ArkvConfig), P(i32), P(i32), i32, i32, P(i32)]
+        L.arkv_tailor_scores.argtypes = [vp, i32, i32, vp, ctypes.c_int64, i32, P(i32), vp]
+        L.arkv_set_tailor_scores.argtypes = [vp, vp, ctypes.c_int64, i32]
         L.arkv_cache_info.argtypes = [vp, i32]
         L.arkv_cache_info.restype = ctypes.c_int32
         L.arkv_prefill_begin.argtypes = [vp, vp, vp, i32, vp, vp]
@@ -269,6 +272,23 @@ class ArkvCache:
                                    self.cfg.quant_bits, _ptr(out), 1 if out.dtype == torch.float32 else 0,
                                    _stream_ptr(stream)), "arkv_decode_step")
         return out
+
+    def arkv_tailor_scores(self, scores, layer0=0, n_layers=None, stream=None) -> int:
+        """Layer-shared states across KV-head shards (include/arkv.h): this cache's score
+        sums for the tailors the next call runs, into scores [max_rows][stride] (fp32,
+        device).  Returns the number of rows written."""
+        n = ctypes.c_int32()
+        n_layers = self.cfg.n_layers - layer0 if n_layers is None else n_layers
+        _ok(lib().arkv_tailor_scores(self.handle, layer0, n_layers, _ptr(scores), scores.shape[1], scores.shape[0],
+                                     ctypes.byref(n), _stream_ptr(stream)), "arkv_tailor_scores")
+        return n.value
+
+    def arkv_set_tailor_scores(self, scores, total_kv_heads):
+        """Exchanged score sums (summed over every shard) for the next call's tailors."""
+        _ok(lib().arkv_set_tailor_scores(self.handle, _ptr(scores) if scores is not None else None,
+                                         scores.shape[1] if scores is not None else 0, total_kv_heads),
+            "arkv_set_tailor_scores")
+        self._ext_scores = scores   # keep the buffer alive until the next call has run
 
     def arkv_unit_counts(self, b, layer):
         n_o, n_q, p, t = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()

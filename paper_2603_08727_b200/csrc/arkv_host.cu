@@ -32,6 +32,12 @@ struct arkv_cache {
   int8_t* st_scratch = nullptr;
   int32_t* src_scratch = nullptr;
   float* sscore = nullptr;
+  // layer-shared states across KV-head shards: score sums exchanged by the caller, consumed
+  // by the next call that runs tailors (arkv_set_tailor_scores)
+  const float* ext_scores = nullptr;
+  int64_t ext_stride = 0;
+  int ext_heads = 0;
+  int prompt_len = 0;  // set by arkv_prefill_begin
   float* pf_partials = nullptr;
   float2* acc_pf = nullptr;
   double* oq_tmp = nullptr;
@@ -538,8 +544,13 @@ static arkv_status run_jobs(arkv_cache* c, std::vector<TailorJob>& jobs, const u
       max_tiles = std::max(max_tiles, tiles);
       if (no > g.cap_o + 0 || jb.n_q_new > g.cap_q) return ARKV_ERR_CAPACITY;
     }
+    SharedScores shs;
+    shs.sscore = c->sscore;
+    shs.ext = c->ext_scores;
+    shs.ext_stride = c->ext_stride;
+    shs.ext_heads = c->ext_heads;
     int nl = launch_tailor(g, tj, n, max_tiles, c->slots, c->meta, c->desc, pk, pv, P, c->acc_pf, c->st_scratch,
-                           c->src_scratch, c->sscore, c->err, s);
+                           c->src_scratch, shs, c->err, s);
     if (nl < 0) return ARKV_ERR_CONFIG;
     c->launches += nl;
     debug_sync(s, "tailor");
@@ -563,6 +574,7 @@ arkv_status arkv_prefill_begin(arkv_cache* c, const void* q_win, const void* k, 
   if (P < g.W + 2) return ARKV_ERR_WINDOW;
   cudaStream_t s = (cudaStream_t)stream;
   const int n_chunks1 = (P + kPfChunkHost - 1) / kPfChunkHost;
+  c->prompt_len = P;
   int nl = launch_prefill_begin(g, (const uint16_t*)q_win, (const uint16_t*)k, P, c->pf_partials, n_chunks1, c->acc_pf,
                                 d_colsum ? d_colsum : c->colsum, s);
   if (nl < 0) return ARKV_ERR_CONFIG;
@@ -638,10 +650,12 @@ arkv_status arkv_prefill_finish(arkv_cache* c, const void* k, const void* v, int
       jb.trig_new = c->trig[bl];
       jb.t_next = P;
       jb.identity = tailor ? 0 : 1;
+      jb.ext_row = (tailor && c->ext_scores) ? bl : -1;  // arkv_tailor_scores rows: every (b, l)
       jobs.push_back(jb);
     }
   }
   arkv_status st = run_jobs(c, jobs, (const uint16_t*)k, (const uint16_t*)v, P, s);
+  c->ext_scores = nullptr;  // consumed
   if (st != ARKV_OK) return st;
   c->prefilled = true;
   return ARKV_OK;
@@ -857,6 +871,77 @@ arkv_status arkv_persist_plan_check(const arkv_config* cfg, const int32_t* n_o, 
   return ok ? ARKV_OK : ARKV_ERR_DEVICE;
 }
 
+arkv_status arkv_tailor_scores(arkv_cache* c, int32_t layer0, int32_t n_layers, float* d_scores, int64_t stride,
+                               int32_t max_rows, int32_t* n_rows, void* stream) {
+  if (!c || !d_scores || !n_rows) return ARKV_ERR_INVALID_ARG;
+  const Geom& g = c->g;
+  if (!g.share) return ARKV_ERR_CONFIG;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<TailorJob> jobs;  // the tailors the next call will run, as score sources
+  int max_ne = 0;
+  if (!c->prefilled) {  // prefill-end tailor (R14): every (b, l), rows = the prompt's eligible tokens
+    const int P = c->prompt_len;
+    if (P <= 0) return ARKV_ERR_SEQUENCE;  // arkv_prefill_begin first (it fills the HH seed)
+    if (P > g.B - g.W) {
+      for (int bl = 0; bl < g.batch * g.L; ++bl)
+        for (int kvh = 0; kvh < g.Hkv; ++kvh) {
+          TailorJob jb{};
+          jb.unit = bl * g.Hkv + kvh;
+          jb.old_slot = -1;
+          jb.n_o_old = P;
+          jb.n_win_old = g.W;
+          jb.ext_row = -1;
+          jobs.push_back(jb);
+        }
+      max_ne = P - g.W;
+    }
+  } else {
+    if (layer0 < 0 || n_layers <= 0 || layer0 + n_layers > g.L) return ARKV_ERR_INVALID_ARG;
+    for (int b = 0; b < g.batch; ++b)
+      for (int l = layer0; l < layer0 + n_layers; ++l) {
+        const int bl = b * g.L + l;
+        if (c->t_next[bl] != c->trig[bl]) continue;
+        for (int kvh = 0; kvh < g.Hkv; ++kvh) {
+          TailorJob jb{};
+          jb.unit = bl * g.Hkv + kvh;
+          jb.old_slot = c->unit_slot[jb.unit];
+          jb.n_o_old = c->n_o[bl];
+          jb.n_q_old = c->n_q[bl];
+          jb.n_win_old = g.W - 1;
+          jb.ext_row = -1;
+          jobs.push_back(jb);
+        }
+        max_ne = std::max(max_ne, c->n_o[bl] - (g.W - 1) + c->n_q[bl]);
+      }
+  }
+  const int rows = (int)jobs.size() / g.Hkv;
+  *n_rows = rows;
+  if (rows == 0) return ARKV_OK;
+  if (rows > max_rows || stride < max_ne) return ARKV_ERR_CAPACITY;
+  const int per = (kMaxJobs / g.Hkv) * g.Hkv;  // whole layers per launch
+  for (size_t i = 0; i < jobs.size(); i += per) {
+    const int n = (int)std::min<size_t>(jobs.size() - i, (size_t)per);
+    TailorJobs tj;
+    std::memset(&tj, 0, sizeof(tj));
+    for (int k = 0; k < n; ++k) tj.j[k] = jobs[i + k];
+    launch_tailor_scores(g, tj, n, max_ne, c->meta, c->acc_pf, d_scores + (int64_t)(i / g.Hkv) * stride, stride,
+                         c->err, s);
+    c->launches += 1;
+  }
+  if (!check_cuda(cudaGetLastError())) return ARKV_ERR_CUDA;
+  return ARKV_OK;
+}
+
+arkv_status arkv_set_tailor_scores(arkv_cache* c, const float* d_scores, int64_t stride, int32_t total_kv_heads) {
+  if (!c) return ARKV_ERR_INVALID_ARG;
+  if (!c->g.share) return ARKV_ERR_CONFIG;
+  if (d_scores && (stride <= 0 || total_kv_heads < c->g.Hkv)) return ARKV_ERR_INVALID_ARG;
+  c->ext_scores = d_scores;
+  c->ext_stride = stride;
+  c->ext_heads = total_kv_heads;
+  return ARKV_OK;
+}
+
 arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, const void* q, const void* k,
                              const void* v, int32_t budget_tokens, int32_t quant_bits, void* out, int32_t out_fp32,
                              void* stream) {
@@ -867,7 +952,7 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   if (!c->prefilled) return ARKV_ERR_SEQUENCE;
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<TailorJob> jobs;
-  int max_tiles = 1, acc_rows = 0;
+  int max_tiles = 1, acc_rows = 0, n_due = 0;
   for (int b = 0; b < g.batch; ++b)
     for (int l = layer0; l < layer0 + n_layers; ++l) {
       const int bl = b * g.L + l;
@@ -892,11 +977,13 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
           jb.trig_new = trig_new;
           jb.t_next = t;
           jb.identity = 0;
+          jb.ext_row = c->ext_scores ? n_due : -1;  // arkv_tailor_scores rows: due (b, l) in order
           jobs.push_back(jb);
         }
         c->n_o[bl] = n_o_after - 1;
         c->n_q[bl] = (int)qn;
         c->trig[bl] = trig_new;
+        ++n_due;
       }
       const int tiles = (c->n_o[bl] + 1 + kTile - 1) / kTile + (c->n_q[bl] + kTile - 1) / kTile;
       max_tiles = std::max(max_tiles, tiles);
@@ -910,8 +997,10 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   if (skip & 2) acc_rows = 0;
   if (!jobs.empty() && !(skip & 1)) {
     arkv_status st = run_jobs(c, jobs, nullptr, nullptr, 0, s);
+    c->ext_scores = nullptr;  // consumed (also when this step runs no tailor: see below)
     if (st != ARKV_OK) return st;
   }
+  c->ext_scores = nullptr;  // exchanged scores serve exactly the call after arkv_tailor_scores
   // split-K fan-out: ~2.6 waves of CTAs (measured at configs[1]: S = 3 beats 2 and 4; more
   // splits cost pipeline fill/drain per CTA and combine reads), never more splits than tiles
   const int n_units_call = g.batch * n_layers * g.Hkv;

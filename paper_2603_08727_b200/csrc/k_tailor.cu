@@ -82,10 +82,46 @@ __device__ __forceinline__ RowView make_rowview(const Geom& g, const TailorJob& 
   return rv;
 }
 
+// Layer-shared states: per group of H_kv consecutive jobs (one (sequence, layer)), the sum
+// over its KV heads of the Eq. 9 score of each eligible row; checks that the heads' rows
+// hold the same positions.
+__global__ void __launch_bounds__(256) tailor_scores_kernel(Geom g, TailorJobs jobs, uint8_t* meta,
+                                                            const float2* __restrict__ acc_pf,
+                                                            float* __restrict__ out, int64_t stride,
+                                                            int32_t* err) {
+  griddep_wait();
+  const int k0 = blockIdx.y * g.Hkv;
+  const TailorJob& j0 = jobs.j[k0];
+  const int n_e = j0.n_o_old - j0.n_win_old + j0.n_q_old;
+  const float invN = 1.0f / (float)(g.G * g.W);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_e) return;
+  float sum = 0.f;
+  int p0 = 0;
+  for (int h = 0; h < g.Hkv; ++h) {
+    const RowView rv = make_rowview(g, jobs.j[k0 + h], meta, acc_pf);
+    float2 a;
+    int p;
+    rv.get(i, a, p);
+    if (h == 0) p0 = p;
+    else if (p != p0) atomicOr(err, kErrIntegrity);
+    sum = __fadd_rn(sum, hh_score(a, invN, g.gamma));
+  }
+  out[(int64_t)blockIdx.y * stride + i] = sum;
+}
+
+void launch_tailor_scores(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_ne, uint8_t* meta,
+                          const float2* acc_pf, float* out, int64_t stride, int32_t* err, cudaStream_t s) {
+  dim3 grid((max(max_ne, 1) + 255) / 256, n_jobs / g.Hkv);
+  launch_pdl(tailor_scores_kernel, grid, dim3(256), 0, s, g, jobs, meta, acc_pf, out, stride, err);
+}
+
 __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs jobs, uint8_t* meta,
                                                              const float2* __restrict__ acc_pf,
                                                              int8_t* __restrict__ st_scratch, int st_stride,
-                                                             float* __restrict__ sscore, int32_t* err) {
+                                                             const float* __restrict__ sscore,
+                                                             const float* __restrict__ ext, int64_t ext_stride,
+                                                             int ext_heads) {
   __shared__ uint32_t hist[2][256];
   __shared__ uint64_t sh_prefix[2];
   __shared__ uint32_t sh_rem[2];
@@ -105,33 +141,24 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
   const float invN = 1.0f / (float)(g.G * g.W);
   const float gamma = g.gamma;
   // layer-shared states (NEXT-3): the score is the mean over the layer's KV
-  // heads, whose jobs are consecutive in this wave (run_jobs aligns waves to layers) and
-  // whose rows hold the same positions in the same order
-  float* ss = g.share ? sscore + (int64_t)blockIdx.x * st_stride : nullptr;
+  // heads — the sum per row comes from tailor_scores_kernel (this cache's heads; the
+  // layer's jobs are consecutive and waves are aligned to layers) or from the sums
+  // exchanged across KV-head shards
+  const float* ssum = nullptr;
+  float nheads = (float)g.Hkv;
   if (g.share) {
-    const int k0 = blockIdx.x - (blockIdx.x % g.Hkv);
-    for (int i = threadIdx.x; i < n_e; i += blockDim.x) {
-      float2 a;
-      int p;
-      rv.get(i, a, p);
-      float sum = 0.f;
-      for (int h = 0; h < g.Hkv; ++h) {
-        const RowView sv = make_rowview(g, jobs.j[k0 + h], meta, acc_pf);
-        float2 ah;
-        int ph;
-        sv.get(i, ah, ph);
-        if (ph != p) atomicOr(err, kErrIntegrity);
-        sum = __fadd_rn(sum, hh_score(ah, invN, gamma));
-      }
-      ss[i] = __fdiv_rn(sum, (float)g.Hkv);
+    if (jb.ext_row >= 0) {
+      ssum = ext + (int64_t)jb.ext_row * ext_stride;
+      nheads = (float)ext_heads;
+    } else {
+      ssum = sscore + (int64_t)(blockIdx.x / g.Hkv) * st_stride;
     }
-    __syncthreads();
   }
   auto key_of = [&](int i) -> uint64_t {
     float2 a;
     int p;
     rv.get(i, a, p);
-    return g.share ? score_key(__ldcg(ss + i), p) : hh_key(a, p, invN, gamma);
+    return g.share ? score_key(__fdiv_rn(__ldcg(ssum + i), nheads), p) : hh_key(a, p, invN, gamma);
   };
 
   const uint32_t kk[2] = {(uint32_t)jb.n_oe, (uint32_t)(jb.n_oe + jb.n_q_new)};
@@ -770,24 +797,32 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
 
 int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_tiles, uint8_t* slots, uint8_t* meta,
                   UnitDesc* desc, const uint16_t* pk, const uint16_t* pv, int P, const float2* acc_pf,
-                  int8_t* st_scratch, int32_t* src_scratch, float* sscore, int32_t* err, cudaStream_t s) {
+                  int8_t* st_scratch, int32_t* src_scratch, const SharedScores& shs, int32_t* err, cudaStream_t s) {
   const int st_stride = max(g.max_pos, g.cap_o) + g.cap_q;
   const int src_stride = g.cap_o + g.cap_q;
+  int extra = 0;
+  if (g.share && jobs.j[0].ext_row < 0) {  // local heads: one score pass per (sequence, layer)
+    int max_ne = 0;
+    for (int k = 0; k < n_jobs; ++k)
+      max_ne = max(max_ne, jobs.j[k].n_o_old - jobs.j[k].n_win_old + jobs.j[k].n_q_old);
+    launch_tailor_scores(g, jobs, n_jobs, max_ne, meta, acc_pf, shs.sscore, st_stride, err, s);
+    extra = 1;
+  }
   launch_pdl(tailor_select_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, meta, acc_pf, st_scratch, st_stride,
-             sscore, err);
+             (const float*)shs.sscore, shs.ext, shs.ext_stride, shs.ext_heads);
   launch_pdl(tailor_scan_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, desc, (const int8_t*)st_scratch, st_stride,
              src_scratch, src_stride, err);
   dim3 grid(max_tiles, n_jobs);
   if (g.layout == ARKV_LAYOUT_FRAG && g.d == mvf::D && g.bits == 4 && std::getenv("ARKV_MOVE_GENERIC") == nullptr) {
     switch (g.ng) {
       case 1: launch_pdl(tailor_move_frag_kernel<1>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride); return 3;
+                         (const int32_t*)src_scratch, src_stride); return 3 + extra;
       case 2: launch_pdl(tailor_move_frag_kernel<2>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride); return 3;
+                         (const int32_t*)src_scratch, src_stride); return 3 + extra;
       case 4: launch_pdl(tailor_move_frag_kernel<4>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride); return 3;
+                         (const int32_t*)src_scratch, src_stride); return 3 + extra;
       case 8: launch_pdl(tailor_move_frag_kernel<8>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride); return 3;
+                         (const int32_t*)src_scratch, src_stride); return 3 + extra;
       default: break;
     }
   }
@@ -803,7 +838,7 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
     break;
   if (g.d == 128) {
     MV_LAUNCH(4, 128)
-    return 3;
+    return 3 + extra;
   }
   switch (vpl) {
     MV_CASE(1)
@@ -815,7 +850,7 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
   }
 #undef MV_CASE
 #undef MV_LAUNCH
-  return 3;
+  return 3 + extra;
 }
 
 }  // namespace arkv

@@ -24,7 +24,7 @@ struct TailorJob {
   int32_t trig_new;   // next tailor position
   int32_t t_next;     // position of the next appended token
   int32_t identity;   // 1: no selection, every old row stays Original (prefill ingest)
-  int32_t pad;
+  int32_t ext_row;    // layer-shared states: row of the exchanged score sums (-1: local heads only)
 };
 struct TailorJobs {
   TailorJob j[kMaxJobs];
@@ -38,9 +38,22 @@ int launch_prefill_finish(const Geom& g, const double* colsum, int P, double* st
                           double stat_eps, cudaStream_t s);
 
 // Tailor of a wave of jobs (D4-D6).
+// Layer-shared states (NEXT-3): the scores of a tailor come either from this cache's KV
+// heads (sscore, written by launch_tailor_scores inside launch_tailor) or from exchanged sums
+// over every shard's heads (ext, ext_stride floats per due (sequence, layer), ext_heads heads).
+struct SharedScores {
+  float* sscore = nullptr;
+  const float* ext = nullptr;
+  int64_t ext_stride = 0;
+  int ext_heads = 0;
+};
 int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_tiles, uint8_t* slots, uint8_t* meta,
                   UnitDesc* desc, const uint16_t* pk, const uint16_t* pv, int P, const float2* acc_pf,
-                  int8_t* st_scratch, int32_t* src_scratch, float* sscore, int32_t* err, cudaStream_t s);
+                  int8_t* st_scratch, int32_t* src_scratch, const SharedScores& shs, int32_t* err, cudaStream_t s);
+// Sums over the jobs' KV heads (consecutive groups of H_kv jobs) of the Eq. 9 scores of the
+// eligible rows: out[group * stride + i].
+void launch_tailor_scores(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_ne, uint8_t* meta,
+                          const float2* acc_pf, float* out, int64_t stride, int32_t* err, cudaStream_t s);
 
 struct DecodeArgs {
   Geom g;

@@ -445,3 +445,53 @@ def test_full_size_configs2_batch8(kernel):
                                        decode_kernel=kernel)
     assert checked >= 8
     assert all(len(u.tailors) >= 1 for o in oras.values() for u in o.units.values())
+
+
+def test_layer_shared_states_kv_head_shards():
+    """NEXT-3 across KV-head shards (collective C3): two caches holding KV heads [0,2) and
+    [2,4) exchange their per-tailor score sums (arkv_tailor_scores -> sum ->
+    arkv_set_tailor_scores, what NCCL all-reduce does across GPUs) and match the unsharded
+    layer-shared cache: token states, codes and outputs."""
+    from paper_2603_08727_b200 import arkv as A
+    sh = Shape(batch=1, n_layers=2, n_q_heads=16, n_kv_heads=4, head_dim=128, prompt_len=1024, window=32)
+    steps = 48
+    qw, k, v = prefill_inputs(sh, seed=19, recipe="margin")
+    mk = lambda hkv, hq: A.make_config(2, hq, hkv, 128, budget_tokens=256, max_positions=1024 + steps + 1,  # noqa: E731
+                                       max_prompt=1024, state_sharing=1)
+    full = A.ArkvCache(mk(4, 16))
+    full.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda())
+    halves = [A.ArkvCache(mk(2, 8)) for _ in range(2)]
+    sl = lambda t, i, hq: t[:, :, hq * i:hq * i + hq].contiguous().cuda()   # noqa: E731
+    parts = []
+    for i, c in enumerate(halves):
+        parts.append(c.arkv_prefill_begin(sl(qw, i, 8), sl(k, i, 2)))
+    colsum = parts[0] + parts[1]                       # C1
+    stride, rows = 2048, 8
+    def exchange(call_layers=None):
+        bufs = [torch.zeros(rows, stride, device="cuda") for _ in range(2)]
+        n = [c.arkv_tailor_scores(bufs[i]) for i, c in enumerate(halves)]
+        assert n[0] == n[1]
+        tot = bufs[0] + bufs[1]                        # C3
+        for c in halves:
+            c.arkv_set_tailor_scores(tot, 4)
+        return n[0]
+    assert exchange() == 2                              # prefill-end tailor of both layers
+    for i, c in enumerate(halves):
+        c.arkv_prefill_finish(sl(k, i, 2), sl(v, i, 2), colsum)
+    n_ex = 0
+    for s in range(steps):
+        q, kn, vn = decode_inputs(sh, s, seed=19, recipe="margin")
+        n_ex += exchange()
+        of = full.arkv_decode_step(q.cuda(), kn.cuda(), vn.cuda())
+        for i, c in enumerate(halves):
+            oh = c.arkv_decode_step(sl(q, i, 8), sl(kn, i, 2), sl(vn, i, 2))
+            torch.testing.assert_close(oh, of[:, :, 8 * i:8 * i + 8], rtol=RTOL, atol=ATOL)
+    assert n_ex >= 2                                     # decode tailors exchanged too
+    for c in halves + [full]:
+        c.arkv_check()
+    for i, c in enumerate(halves):
+        for l in range(2):
+            for h in range(2):
+                e, r = c.arkv_export_unit(0, l, h), full.arkv_export_unit(0, l, 2 * i + h)
+                for key in ("state", "q_k", "k_scale", "o_v"):
+                    np.testing.assert_array_equal(e[key], r[key])
