@@ -73,9 +73,11 @@ def compare_unit(gpu, ora, b, l, kvh, where=""):
         np.testing.assert_array_equal(e[key][q], r[key][q], err_msg=key + " " + tag)
 
 
-def run_parity(sh: Shape, budget, steps, seed=0, recipe="margin", rho=None, check_every=1, **kw):
+def run_parity(sh: Shape, budget, steps, seed=0, recipe="margin", rho=None, check_every=1, mutate=None, **kw):
     gpu, ora, ocfg = make_pair(sh, budget, steps=steps, **kw)
     qw, k, v = prefill_inputs(sh, seed=seed, recipe=recipe)
+    if mutate is not None:
+        mutate(qw, k, v)
     stats, oq, rho_gpu = gpu.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda(), rho_override=rho)
     ora.prefill(_np(qw), _np(k), _np(v), rho_override=rho_gpu)
     gpu.arkv_check()
@@ -495,3 +497,33 @@ def test_layer_shared_states_kv_head_shards():
                 e, r = c.arkv_export_unit(0, l, h), full.arkv_export_unit(0, l, 2 * i + h)
                 for key in ("state", "q_k", "k_scale", "o_v"):
                     np.testing.assert_array_equal(e[key], r[key])
+
+
+
+@pytest.mark.parametrize("layout", [1, 2])
+def test_rho_zero_all_kept_tokens_quantized(layout):
+    """rho = 0 (the Base_quant regime): every kept eligible token is Quantized (n_oe = 0)."""
+    r = run_parity(MID, budget=512, steps=48, seed=12, rho=[[0.0, 0.0]], layout=layout, bits=4, g=128,
+                   check_every=16)
+    for u in r["ora"].units.values():
+        assert all(t[1] == MID.window for t in u.tailors)      # only the window stays Original
+
+
+def test_minimal_budget_frequent_tailors():
+    """B = 2W + 1, the smallest budget R14 allows: a tailor every W + 1 steps keeping one
+    eligible token, no room left for Quantized tokens (schedule (32, 65, 98, ...))."""
+    sh = Shape(batch=1, n_layers=1, n_q_heads=8, n_kv_heads=2, head_dim=128, prompt_len=300, window=32)
+    r = run_parity(sh, budget=65, steps=100, seed=14, rho=[[0.5]], layout=2, bits=4, g=128, check_every=10)
+    assert min(len(u.tailors) for u in r["ora"].units.values()) >= 4
+
+
+def test_constant_groups_quantize_to_scale_one():
+    """Tokens whose K/V groups are constant (R23: s = 1, codes 0, z = the value; symmetric
+    all-zero groups: s = 1) survive the tailor bit-exactly and attend correctly."""
+    def mutate(qw, k, v):
+        k[:, :, :, 100:140, :64] = 0.25          # first group (g = 64) constant for 40 tokens
+        v[:, :, :, 100:140, 64:] = -0.5
+        v[:, :, :, 200:220, :] = 0.0             # whole rows zero
+    for mode in ("asym", "sym"):
+        run_parity(MID, budget=512, steps=24, seed=15, rho=[[0.3, 0.6]], layout=2, bits=4, g=64, mode=mode,
+                   check_every=24, mutate=mutate)
