@@ -953,6 +953,9 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<TailorJob> jobs;
   int max_tiles = 1, acc_rows = 0, n_due = 0;
+  HhPlan hh;  // (sequence, layer) pairs in their HH window this step (fused combine)
+  hh.n = 0;
+  bool hh_fit = true;
   for (int b = 0; b < g.batch; ++b)
     for (int l = layer0; l < layer0 + n_layers; ++l) {
       const int bl = b * g.L + l;
@@ -987,8 +990,14 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
       }
       const int tiles = (c->n_o[bl] + 1 + kTile - 1) / kTile + (c->n_q[bl] + kTile - 1) / kTile;
       max_tiles = std::max(max_tiles, tiles);
-      if (t >= c->trig[bl] - g.W && t < c->trig[bl])  // HH accumulation step (R19)
-        acc_rows = std::max(acc_rows, c->n_o[bl] + 1 + c->n_q[bl]);
+      if (t >= c->trig[bl] - g.W && t < c->trig[bl]) {  // HH accumulation step (R19)
+        const int rows = c->n_o[bl] + 1 + c->n_q[bl];
+        acc_rows = std::max(acc_rows, rows);
+        if (hh.n < kMaxHhEntries)
+          hh.e[hh.n++] = make_int4(b * n_layers + (l - layer0), rows, t == c->trig[bl] - g.W ? 1 : 0, c->n_q[bl]);
+        else
+          hh_fit = false;
+      }
     }
   // ARKV_TIMING_SKIP (timing experiments only; results are wrong): bit 0 skips the tailor
   // launches, bit 1 the HH accumulation, bit 2 the split combine, so a bench run isolates
@@ -1029,6 +1038,11 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
     c->ev_used++;
   }
   PlanArgs pa;
+  static const bool fuse_hh = !std::getenv("ARKV_FUSE_HH") || std::atoi(std::getenv("ARKV_FUSE_HH")) != 0;
+  if (acc_rows > 0 && hh_fit && fuse_hh && !c->persist) {
+    hh.n_units = g.batch * n_layers * g.Hkv;
+    pa.hh = &hh;
+  }
   PersistPlan plan;
   if (c->persist) {
     build_plan(c, layer0, n_layers, 2 * c->num_sms, &plan);

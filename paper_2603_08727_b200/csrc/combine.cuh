@@ -10,41 +10,74 @@
 
 namespace arkv {
 
+// Merged max M (log2 domain), sum L and — WITH_O — output element o[x] of head h over the
+// S split partials.  The (m, l, o) of up to kB splits are loaded as one batch of
+// independent loads: one memory round trip per kB splits instead of three dependent ones
+// (max, sum, output).  For S <= kB the order (global max, then the sums in split order) is
+// the plain reduction's.  The HH rows of the fused combine call it without O and get the
+// combine's M and L bit for bit.
+template <int G, bool WITH_O>
+__device__ __forceinline__ void merge_splits(const float* part, int h, int x, int S, int d, float& M, float& L,
+                                             float& O) {
+  constexpr int kB = 8;
+  M = -INFINITY;
+  L = 0.f;
+  O = 0.f;
+  for (int s0 = 0; s0 < S; s0 += kB) {
+    float m[kB], l[kB], o[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int s = s0 + j;
+      const float* p = part + (s * G + h) * (d + 2);
+      m[j] = s < S ? __ldcg(p) : -INFINITY;
+      l[j] = s < S ? __ldcg(p + 1) : 0.f;
+      o[j] = (WITH_O && s < S) ? __ldcg(p + 2 + x) : 0.f;
+    }
+    float bm = M;
+#pragma unroll
+    for (int j = 0; j < kB; ++j) bm = fmaxf(bm, m[j]);
+    if (bm == -INFINITY) continue;
+    if (M != -INFINITY) {
+      const float c = exp2f(M - bm);
+      L *= c;
+      if (WITH_O) O *= c;
+    }
+    M = bm;
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      if (m[j] != -INFINITY) {
+        const float w = exp2f(m[j] - M);
+        L += l[j] * w;
+        if (WITH_O) O += o[j] * w;
+      }
+    }
+  }
+}
+
 template <int G>
 __device__ __forceinline__ void combine_unit(const DecodeArgs& a, int u, int b, int li, int kvh, const UnitDesc& dsc,
-                                             float* sM, float* sIL) {
+                                             float* /*sM*/, float* /*sIL*/) {
   const Geom& g = a.g;
   const int d = g.d;
   const int S = a.n_splits;
   const float* part = a.partials + (int64_t)u * a.max_splits * G * (d + 2);
-  if (threadIdx.x < G) {
-    const int h = threadIdx.x;
-    float M = -INFINITY;
-    for (int s = 0; s < S; ++s) M = fmaxf(M, __ldcg(part + (s * G + h) * (d + 2)));
-    float L = 0.f;
-    for (int s = 0; s < S; ++s) {
-      const float ms = __ldcg(part + (s * G + h) * (d + 2));
-      if (ms != -INFINITY) L += __ldcg(part + (s * G + h) * (d + 2) + 1) * exp2f(ms - M);
-    }
-    sM[h] = M;
-    sIL[h] = 1.0f / L;
-    a.mstat[((int64_t)u * G + h) * 2 + 0] = M;
-    a.mstat[((int64_t)u * G + h) * 2 + 1] = 1.0f / L;
-  }
-  __syncthreads();
   const int64_t obase = ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * G) * d;
+  // one thread per (head, dim); each merges its head's split statistics itself (redundant
+  // across the head's d threads, but no shared-memory round and no __syncthreads)
   for (int idx = threadIdx.x; idx < G * d; idx += blockDim.x) {
     const int h = idx / d, x = idx % d;
-    float O = 0.f;
-    for (int s = 0; s < S; ++s) {
-      const float ms = __ldcg(part + (s * G + h) * (d + 2));
-      if (ms != -INFINITY) O += __ldcg(part + (s * G + h) * (d + 2) + 2 + x) * exp2f(ms - sM[h]);
-    }
-    O *= sIL[h];
+    float M, L, O;
+    merge_splits<G, true>(part, h, x, S, d, M, L, O);
+    const float IL = 1.0f / L;
+    O *= IL;
     if (a.out_fp32)
       ((float*)a.out)[obase + idx] = O;
     else
       ((uint16_t*)a.out)[obase + idx] = f_to_bf16_rne(O);
+    if (x == 0) {
+      a.mstat[((int64_t)u * G + h) * 2 + 0] = M;
+      a.mstat[((int64_t)u * G + h) * 2 + 1] = IL;
+    }
   }
   if (threadIdx.x == 0) {
     UnitDesc nd = dsc;

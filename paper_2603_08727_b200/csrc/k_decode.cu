@@ -285,6 +285,85 @@ __global__ void __launch_bounds__(256) decode_hh_acc(DecodeArgs a) {
   }
 }
 
+// one combine thread per (head, dim) up to 1024 (measured: latency-bound otherwise)
+static int combine_threads(const Geom& g) { return std::min(1024, std::max(128, (g.G * g.d + 31) / 32 * 32)); }
+
+// Split combine with the step's HH accumulation in the same grid (saves the separate
+// decode_hh_acc launch and its drain).  Combine blocks as decode_combine; an HH block
+// recomputes its unit's merged (M, 1/L) with the combine's own code (bit-identical), then
+// folds rows [chunk * R, chunk * R + R) exactly as decode_hh_acc does.
+constexpr int kHhRowsPerThread = 2;
+template <int G>
+__global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const HhPlan hp) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const Geom& g = a.g;
+  if ((int)blockIdx.x < hp.n_units) {
+    int b, li, kvh, u;
+    unit_of(a, blockIdx.x, b, li, kvh, u);
+    const UnitDesc dsc = a.desc[u];
+    combine_unit<G>(a, u, b, li, kvh, dsc, nullptr, nullptr);
+    return;
+  }
+  const int idx = blockIdx.x - hp.n_units;
+  const int per_e = g.Hkv * hp.nchunk;
+  const int4 en = hp.e[idx / per_e];
+  const int kvh = (idx % per_e) / hp.nchunk, chunk = idx % hp.nchunk;
+  const int R = blockDim.x * kHhRowsPerThread;
+  const int n_rows = en.y, r0 = chunk * R;
+  if (r0 >= n_rows) return;
+  const int b = en.x / a.n_layers, li = en.x % a.n_layers;
+  const int u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
+  __shared__ float sM[G], sIL[G];
+  if ((int)threadIdx.x < G) {
+    const float* part = a.partials + (int64_t)u * a.max_splits * G * (g.d + 2);
+    float M, L, O;
+    merge_splits<G, false>(part, threadIdx.x, 0, a.n_splits, g.d, M, L, O);
+    sM[threadIdx.x] = M;
+    sIL[threadIdx.x] = 1.0f / L;
+  }
+  __syncthreads();
+  const bool first = en.z != 0;
+  const int n_o = n_rows - en.w;  // Original rows, the appended token included
+  // the slot is not changed by the combine's descriptor advance
+  const SlotMeta sm = slot_meta(a.meta, g, a.desc[u].slot);
+  const int row_stride = g.cap_o + g.cap_q;
+  const int r1 = min(n_rows, r0 + R);
+  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const bool isq = i >= n_o;
+    const int ridx = isq ? g.cap_o + (i - n_o) : i;
+    float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const float p = exp2f(a.logits[((int64_t)u * G + h) * row_stride + ridx] - sM[h]) * sIL[h];
+      a1 += p;
+      a2 += p * p;
+    }
+    float2* ap = isq ? &sm.acc_q[i - n_o] : &sm.acc_o[i];
+    if (first) {
+      *ap = make_float2(a1, a2);
+    } else {
+      const float2 c = *ap;
+      *ap = make_float2(c.x + a1, c.y + a2);
+    }
+  }
+}
+
+void launch_decode_combine_hh(const DecodeArgs& a, const HhPlan& hp, int max_rows, cudaStream_t s) {
+  HhPlan p = hp;
+  const int threads = combine_threads(a.g);
+  const int R = threads * kHhRowsPerThread;
+  p.nchunk = std::max(1, (max_rows + R - 1) / R);
+  const dim3 grid(p.n_units + p.n * a.g.Hkv * p.nchunk);
+  switch (a.g.G) {
+    case 1: launch_pdl(decode_combine_hh<1>, grid, dim3(threads), 0, s, a, p); break;
+    case 2: launch_pdl(decode_combine_hh<2>, grid, dim3(threads), 0, s, a, p); break;
+    case 4: launch_pdl(decode_combine_hh<4>, grid, dim3(threads), 0, s, a, p); break;
+    case 8: launch_pdl(decode_combine_hh<8>, grid, dim3(threads), 0, s, a, p); break;
+    default: break;
+  }
+}
+
 void launch_decode_hh_acc(const DecodeArgs& a, int n_units_call, int max_rows, cudaStream_t s) {
   dim3 grid((max_rows + 255) / 256, n_units_call);
   switch (a.g.G) {
@@ -298,11 +377,9 @@ void launch_decode_hh_acc(const DecodeArgs& a, int n_units_call, int max_rows, c
 
 // k_decode_fast.cu: returns -1 if the cache is not eligible.
 int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
-                       const PersistPlan* plan);
+                       const PersistPlan* plan, const HhPlan* hh, int acc_rows);
 void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s);
 
-// one combine thread per (head, dim) up to 1024 (measured: latency-bound otherwise)
-static int combine_threads(const Geom& g) { return std::min(1024, std::max(128, (g.G * g.d + 31) / 32 * 32)); }
 
 template <int G>
 static void launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
@@ -379,8 +456,9 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
   const int n_units_call = g.batch * n_layers * g.Hkv;
   int n = -1;
   if (fast) {
-    n = launch_decode_fast(a, n_units_call, s, ev0, ev1, plan.plan);
+    n = launch_decode_fast(a, n_units_call, s, ev0, ev1, plan.plan, acc_rows > 0 ? plan.hh : nullptr, acc_rows);
     if (n < 0) return n;
+    if (n >= 100) return n - 100;  // the combine folded the HH accumulation
   } else {
     switch (g.G) {
       case 1: launch_g<1>(a, n_units_call, s, ev0, ev1); break;

@@ -131,6 +131,24 @@ __device__ __forceinline__ void unpack8(uint32_t w, uint32_t (&x)[4]) {
   x[2] = hsub2_1024(lop3_mask_or(w8, 0x000F000Fu, 0x64006400u));
   x[3] = hsub2_1024(lop3_mask_or(w8, 0x00F000F0u, 0x64006400u));
 }
+// The same four code pairs as fp16 SUBNORMALS: a nibble masked into the low mantissa bits
+// (exponent field 0) is exactly c * 2^-24 (16c * 2^-24 for the odd nibbles), so one LOP3
+// per two codes gives an exactly scaled A operand — no "- 1024".  The tensor core keeps
+// fp16 subnormal inputs, and every product and fp32 partial sum of the contraction is the
+// exact-unpack value times 2^-24, so the caller's 2^24 factor (folded into the k scale)
+// restores bit-identical logits.
+__device__ __forceinline__ void unpack8_sub(uint32_t w, uint32_t (&x)[4]) {
+  const uint32_t w8 = w >> 8;
+  x[0] = w & 0x000F000Fu;
+  x[1] = w & 0x00F000F0u;
+  x[2] = w8 & 0x000F000Fu;
+  x[3] = w8 & 0x00F000F0u;
+}
+#ifndef ARKV_QK_SUB
+#define ARKV_QK_SUB 1
+#endif
+constexpr bool kQkSub = ARKV_QK_SUB != 0;
+constexpr float kSubScale = 16777216.0f;  // 2^24
 // Two e4m3 codes (the low / high 16 bits of w) -> f16x2 (lower code -> lower half).
 __device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint32_t v16) {
   const __half2_raw h = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(v16 & 0xFFFFu), __NV_E4M3);
@@ -391,8 +409,13 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
 #pragma unroll
       for (int jp = 0; jp < 4; ++jp) {
         uint32_t x[4], y[4];
-        unpack8(word(r0, jp), x);
-        unpack8(word(r1, jp), y);
+        if (kQkSub) {
+          unpack8_sub(word(r0, jp), x);
+          unpack8_sub(word(r1, jp), y);
+        } else {
+          unpack8(word(r0, jp), x);
+          unpack8(word(r1, jp), y);
+        }
         const int gr = (jp * 32) / (D / NG);
         mma_f16(acc[gr], x[0], y[0], x[1], y[1], f.qh[2 * jp][0], f.qh[2 * jp][1]);
         mma_f16(acc[gr], x[2], y[2], x[3], y[3], f.qh[2 * jp + 1][0], f.qh[2 * jp + 1][1]);
@@ -410,8 +433,9 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
             kz = -8.f * ks;
             vz = -8.f * vs;
           }
-          l0 += ks * acc[gr][hh * 2 + 0] + kz * f.qsum[0][gr];
-          l1 += ks * acc[gr][hh * 2 + 1] + kz * f.qsum[1][gr];
+          const float ksc = kQkSub ? ks * kSubScale : ks;  // exact: power-of-two factor
+          l0 += ksc * acc[gr][hh * 2 + 0] + kz * f.qsum[0][gr];
+          l1 += ksc * acc[gr][hh * 2 + 1] + kz * f.qsum[1][gr];
           // PV runs on the raw magic-number codes (1024 + c for rows g, 1024 + 16c for
           // rows g+8, whose P' carries 1/16): the offset is removed here, in the z term
           zv[mt][hh][gr] = kPvRaw ? vz - (hh ? 64.f : 1024.f) * vs : vz;
@@ -1318,8 +1342,11 @@ bool decode_fast_available(const Geom& g) {
 
 void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s);  // k_decode.cu
 
+void launch_decode_combine_hh(const DecodeArgs& a, const HhPlan& hp, int max_rows, cudaStream_t s);  // k_decode.cu
+
+// Returns the launches issued, + 100 when the step's HH accumulation ran inside the combine.
 int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
-                       const PersistPlan* plan) {
+                       const PersistPlan* plan, const HhPlan* hh, int acc_rows) {
   if (!decode_fast_available(a.g)) return -1;
   if (plan) {  // persistent range-partitioned kernel + its combine
     switch (a.g.G) {
@@ -1343,6 +1370,10 @@ int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
   // ARKV_TIMING_SKIP bit 2 (timing experiments only, results wrong): no combine
   static const int skip = std::getenv("ARKV_TIMING_SKIP") ? std::atoi(std::getenv("ARKV_TIMING_SKIP")) : 0;
   if (skip & 4) return 1;
+  if (hh) {
+    launch_decode_combine_hh(a, *hh, acc_rows, s);
+    return 102;
+  }
   launch_decode_combine(a, n_units_call, s);
   return 2;
 }

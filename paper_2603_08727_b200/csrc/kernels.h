@@ -104,7 +104,22 @@ struct PersistPlan {
   int4 cta[2][kPlanMaxCtas];
   int ue[2][kPlanMaxCtas];  // unit of the range's last item
 };
+// Heavy-hitter accumulation fused into the split combine (D3; R19): the (sequence, layer)
+// pairs of a call whose step lies in their HH window, from the host's count schedule (the
+// same test as the device's, so no descriptor read races the combine's advance).  Passed
+// by value as a kernel parameter.  Blocks [0, n_units) of decode_combine_hh merge the
+// split partials; the others each take kRows rows of one (entry, KV head).
+constexpr int kMaxHhEntries = 256;
+struct HhPlan {
+  int n;           // entries
+  int n_units;     // units of the call (= combine blocks)
+  int nchunk;      // row chunks per (entry, KV head)
+  int pad_;
+  int4 e[kMaxHhEntries];  // x = b * n_layers + li; y = rows (n_o after the append + n_q);
+                          // z = 1 on the window's first step (acc := sample); w = n_q
+};
 struct PlanArgs {
+  const HhPlan* hh = nullptr;         // fused HH plan (split-K fast kernel), or nullptr
   const PersistPlan* plan = nullptr;  // host plan, or nullptr: split-K kernels
   float* pparts = nullptr;
   int4* pcta = nullptr;
