@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def comp(src):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-        cmd = [cc, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        # ARKV_NVCC_FLAGS: extra defines for A/B builds of compile-time switches (measurement only)
+        cmd = [cc, *ARCH, *FLAGS, *os.environ.get("ARKV_NVCC_FLAGS", "").split(), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")

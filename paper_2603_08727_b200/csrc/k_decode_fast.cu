@@ -149,6 +149,12 @@ __device__ __forceinline__ void unpack8_sub(uint32_t w, uint32_t (&x)[4]) {
 #endif
 constexpr bool kQkSub = ARKV_QK_SUB != 0;
 constexpr float kSubScale = 16777216.0f;  // 2^24
+// QK^T of a tile as two independent accumulator chains (halves the MMA dependency depth;
+// the fp32 sum order of the logits changes by one final add)
+#ifndef ARKV_QK_SPLIT
+#define ARKV_QK_SPLIT 1
+#endif
+constexpr bool kQkSplit = ARKV_QK_SPLIT != 0;
 // Two e4m3 codes (the low / high 16 bits of w) -> f16x2 (lower code -> lower half).
 __device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint32_t v16) {
   const __half2_raw h = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(v16 & 0xFFFFu), __NV_E4M3);
@@ -349,16 +355,18 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
   if (!isq) {
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      // two accumulators per m-tile (kQkSplit): the 8 MMAs form two dependent chains of 4
+      float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
       for (int qd = 0; qd < 4; ++qd) {
         const uint4 r0 = lds128(tb + (((mt * 2 + 0) * 4 + qd) * 32 + lane) * 16);
         const uint4 r1 = lds128(tb + (((mt * 2 + 1) * 4 + qd) * 32 + lane) * 16);
-        mma_bf16(acc, r0.x, r1.x, r0.y, r1.y, f.qb[2 * qd][0], f.qb[2 * qd][1]);
-        mma_bf16(acc, r0.z, r1.z, r0.w, r1.w, f.qb[2 * qd + 1][0], f.qb[2 * qd + 1][1]);
+        float(&ac)[4] = acc[kQkSplit ? (qd & 1) : 0];
+        mma_bf16(ac, r0.x, r1.x, r0.y, r1.y, f.qb[2 * qd][0], f.qb[2 * qd][1]);
+        mma_bf16(ac, r0.z, r1.z, r0.w, r1.w, f.qb[2 * qd + 1][0], f.qb[2 * qd + 1][1]);
       }
 #pragma unroll
-      for (int e = 0; e < 4; ++e) lg[mt][e] = acc[e] * c2;
+      for (int e = 0; e < 4; ++e) lg[mt][e] = (kQkSplit ? acc[0][e] + acc[1][e] : acc[0][e]) * c2;
     }
   } else if (F8) {
     // fp8 e4m3 codes: one cvt.rn.f16x2.e4m3x2 per byte pair gives the f16 A fragment;
@@ -399,11 +407,11 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
     const float* sc = (const float*)(tb + 32 * D);  // [row][grp][k_scale, k_zero, v_scale, v_zero]
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
-      float acc[NG][4];
+      float acc[NG][4], acc2[NG][4];  // acc2: odd jp when two jp share a group (kQkSplit)
 #pragma unroll
       for (int gr = 0; gr < NG; ++gr)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[gr][e] = 0.f;
+        for (int e = 0; e < 4; ++e) acc[gr][e] = acc2[gr][e] = 0.f;
       const uint4 r0 = lds128(tb + ((mt * 2 + 0) * 32 + lane) * 16);
       const uint4 r1 = lds128(tb + ((mt * 2 + 1) * 32 + lane) * 16);
 #pragma unroll
@@ -417,8 +425,15 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
           unpack8(word(r1, jp), y);
         }
         const int gr = (jp * 32) / (D / NG);
-        mma_f16(acc[gr], x[0], y[0], x[1], y[1], f.qh[2 * jp][0], f.qh[2 * jp][1]);
-        mma_f16(acc[gr], x[2], y[2], x[3], y[3], f.qh[2 * jp + 1][0], f.qh[2 * jp + 1][1]);
+        float(&ac)[4] = (kQkSplit && NG <= 2 && (jp & 1)) ? acc2[gr] : acc[gr];
+        mma_f16(ac, x[0], y[0], x[1], y[1], f.qh[2 * jp][0], f.qh[2 * jp][1]);
+        mma_f16(ac, x[2], y[2], x[3], y[3], f.qh[2 * jp + 1][0], f.qh[2 * jp + 1][1]);
+      }
+      if (kQkSplit && NG <= 2) {
+#pragma unroll
+        for (int gr = 0; gr < NG; ++gr)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[gr][e] += acc2[gr][e];
       }
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
@@ -626,7 +641,7 @@ __device__ __forceinline__ void acc_reduce_rows(Acc<NG>& s) {
 }
 
 template <int G, int NG, int C, int SPW, bool F8>
-__global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 65536) ? 2 : 1)
+__global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kStageBytes) ? 2 : 1)
     decode_fast_kernel(DecodeArgs a) {
   constexpr int kConsumers = C;
   constexpr int kStages = C * SPW;
@@ -894,27 +909,37 @@ static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
   if (ev1) cudaEventRecord(ev1, s);
 }
 
-// Default pipeline shape: 4 consumer warps x 1 stage (64 KB ring, 2 CTAs/SM).  For the
-// paper's shape (G = 4, one group) a few alternatives are selectable for measurement
-// with ARKV_FAST_CFG=C,SPW (4,1 | 4,2 | 6,2 | 4,3 | 8,1).
+// Default pipeline shape: 3 consumer warps x 2 stages (96 KB ring, 2 CTAs/SM): every
+// consumer warp has its next item in flight while it computes the current one (with one
+// stage per warp, the warp waited a full HBM round trip per item: 21 % of the stall
+// samples of the Base_quant profile).  Measured at configs[1]: kernel 0.1693 -> 0.1565 ms
+// vs 4 x 1.  For the paper's shape (G = 4, one group) alternatives are selectable for
+// measurement with ARKV_FAST_CFG=C,SPW (4,1 | 4,2 | 6,2 | 4,3 | 8,1 | 2,2 | 2,3).
 template <int G, int NG>
 static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
   if (a.g.mode == ARKV_QUANT_FP8) {
-    launch_cfg<G, NG, 4, 1, true>(a, n_units_call, s, ev0, ev1);
+    const char* e = std::getenv("ARKV_FAST_CFG");
+    if (e && e[0] == '4')
+      launch_cfg<G, NG, 4, 1, true>(a, n_units_call, s, ev0, ev1);
+    else
+      launch_cfg<G, NG, 3, 2, true>(a, n_units_call, s, ev0, ev1);
     return;
   }
   if (G == 4 && NG == 1) {
     const char* e = std::getenv("ARKV_FAST_CFG");
-    const int cfg = e ? (e[0] - '0') * 10 + (e[2] - '0') : 41;
+    const int cfg = e ? (e[0] - '0') * 10 + (e[2] - '0') : 32;
     switch (cfg) {
       case 42: launch_cfg<G, NG, 4, 2>(a, n_units_call, s, ev0, ev1); return;
       case 62: launch_cfg<G, NG, 6, 2>(a, n_units_call, s, ev0, ev1); return;
       case 43: launch_cfg<G, NG, 4, 3>(a, n_units_call, s, ev0, ev1); return;
       case 81: launch_cfg<G, NG, 8, 1>(a, n_units_call, s, ev0, ev1); return;
+      case 41: launch_cfg<G, NG, 4, 1>(a, n_units_call, s, ev0, ev1); return;
+      case 22: launch_cfg<G, NG, 2, 2>(a, n_units_call, s, ev0, ev1); return;
+      case 23: launch_cfg<G, NG, 2, 3>(a, n_units_call, s, ev0, ev1); return;
       default: break;
     }
   }
-  launch_cfg<G, NG, 4, 1>(a, n_units_call, s, ev0, ev1);
+  launch_cfg<G, NG, 3, 2>(a, n_units_call, s, ev0, ev1);
 }
 
 template <int G>
