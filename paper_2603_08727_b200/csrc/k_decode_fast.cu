@@ -1024,12 +1024,15 @@ struct Walker {
     }
   }
 };
+// Ring of C x kPersistSpw stages: item j -> stage j % (C SPW), consumer warp j % C, so each
+// stage has a single owner warp that waits on its barriers strictly in phase order.
 template <int C>
 struct PSmem {
-  uint8_t ring[C][kStageBytes];
-  uint64_t full[C];
-  uint64_t empty[C];
-  int4 info[C][2];  // per stage, written by the producer: (ul, u, k, phase), (n_o, n_q, tiles_q, accm)
+  static constexpr int kSt = C * kPersistSpw;
+  uint8_t ring[kSt][kStageBytes];
+  uint64_t full[kSt];
+  uint64_t empty[kSt];
+  int4 info[kSt][2];  // per stage, written by the producer: (ul, u, k, phase), (n_o, n_q, tiles_q, accm)
 };
 
 template <int G, int NG, bool F8>
@@ -1050,7 +1053,7 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
   const bool sym = g.mode == ARKV_QUANT_SYM;
   const int n_units_call = g.batch * a.n_layers * g.Hkv;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < C; ++i) {
+    for (int i = 0; i < PSmem<C>::kSt; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], 1);
     }
@@ -1079,8 +1082,9 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
         // the CTAs holding a unit's first and last item of the phase, for the combine
         if (w.k == 0) a.pcover[(f * 2 + 0) * n_units_call + w.ul] = c;
         if (w.k == p.items - 1) a.pcover[(f * 2 + 1) * n_units_call + w.ul] = c;
-        const int st = j % C;
-        if (j >= C) mbar_wait(&sm.empty[st], ((j / C) - 1) & 1);
+        constexpr int NS = PSmem<C>::kSt;
+        const int st = j % NS;
+        if (j >= NS) mbar_wait(&sm.empty[st], ((j / NS) - 1) & 1);
         sm.info[st][0] = make_int4(w.ul, p.u, w.k, f);
         sm.info[st][1] = make_int4(p.n_o, p.n_q, p.tiles_q, p.accm ? 1 : 0);
         uint8_t* slot = a.slots + (int64_t)p.slot * g.slot_bytes;
@@ -1161,8 +1165,9 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
     }
   };
   for (int j = warp; j < n_work; j += C) {
-    const int st = j % C;
-    mbar_wait(&sm.full[st], (j / C) & 1);
+    constexpr int NS = PSmem<C>::kSt;
+    const int st = j % NS;
+    mbar_wait(&sm.full[st], (j / NS) & 1);
     __syncwarp();  // mma/movmatrix are .aligned
     const int4 i0 = sm.info[st][0], i1 = sm.info[st][1];
     if (i0.x != cur) {

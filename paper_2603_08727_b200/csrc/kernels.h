@@ -92,7 +92,8 @@ struct DecodeArgs {
 // so every CTA gets the same bytes of each kind (the kinds cost differently: HBM-bound vs.
 // ALU-heavy).  A CTA streams its phase-0 range, then its phase-1 range; the kernel walks
 // unit boundaries itself from the descriptors.
-constexpr int kPersistConsumers = 4;
+constexpr int kPersistConsumers = 3;
+constexpr int kPersistSpw = 2;  // ring stages per consumer warp (next item in flight while computing)
 constexpr int kPlanMaxCtas = 320;  // 2 CTAs/SM x <= 160 SMs
 // partial slots one combine merges (C per covering CTA and phase)
 constexpr int kMaxUnitParts = 512;
