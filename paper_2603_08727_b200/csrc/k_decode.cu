@@ -292,7 +292,7 @@ static int combine_threads(const Geom& g) { return std::min(1024, std::max(128, 
 // decode_hh_acc launch and its drain).  Combine blocks as decode_combine; an HH block
 // recomputes its unit's merged (M, 1/L) with the combine's own code (bit-identical), then
 // folds rows [chunk * R, chunk * R + R) exactly as decode_hh_acc does.
-constexpr int kHhRowsPerThread = 2;
+constexpr int kHhRowsPerThread = 4;
 template <int G>
 __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const HhPlan hp) {
   griddep_wait();
@@ -314,6 +314,26 @@ __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const Hh
   if (r0 >= n_rows) return;
   const int b = en.x / a.n_layers, li = en.x % a.n_layers;
   const int u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
+  const bool first = en.z != 0;
+  const int n_o = n_rows - en.w;  // Original rows, the appended token included
+  // the slot is not changed by the combine's descriptor advance
+  const SlotMeta sm = slot_meta(a.meta, g, a.desc[u].slot);
+  const int row_stride = g.cap_o + g.cap_q;
+  // every row load of the thread is issued before the merged statistics are needed (the
+  // logits do not depend on them): kHhRowsPerThread rows x (G logits + acc) in flight
+  float lg[kHhRowsPerThread][G];
+  float2 ac[kHhRowsPerThread];
+#pragma unroll
+  for (int k = 0; k < kHhRowsPerThread; ++k) {
+    const int i = r0 + threadIdx.x + k * blockDim.x;
+    const bool ok = i < n_rows;
+    const bool isq = i >= n_o;
+    const int ridx = isq ? g.cap_o + (i - n_o) : i;
+#pragma unroll
+    for (int h = 0; h < G; ++h) lg[k][h] = ok ? __ldcs(a.logits + ((int64_t)u * G + h) * row_stride + ridx) : 0.f;
+    ac[k] = make_float2(0.f, 0.f);
+    if (ok && !first) ac[k] = isq ? sm.acc_q[i - n_o] : sm.acc_o[i];
+  }
   __shared__ float sM[G], sIL[G];
   if ((int)threadIdx.x < G) {
     const float* part = a.partials + (int64_t)u * a.max_splits * G * (g.d + 2);
@@ -323,29 +343,19 @@ __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const Hh
     sIL[threadIdx.x] = 1.0f / L;
   }
   __syncthreads();
-  const bool first = en.z != 0;
-  const int n_o = n_rows - en.w;  // Original rows, the appended token included
-  // the slot is not changed by the combine's descriptor advance
-  const SlotMeta sm = slot_meta(a.meta, g, a.desc[u].slot);
-  const int row_stride = g.cap_o + g.cap_q;
-  const int r1 = min(n_rows, r0 + R);
-  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-    const bool isq = i >= n_o;
-    const int ridx = isq ? g.cap_o + (i - n_o) : i;
+#pragma unroll
+  for (int k = 0; k < kHhRowsPerThread; ++k) {
+    const int i = r0 + threadIdx.x + k * blockDim.x;
+    if (i >= n_rows) break;
     float a1 = 0.f, a2 = 0.f;
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-      const float p = exp2f(a.logits[((int64_t)u * G + h) * row_stride + ridx] - sM[h]) * sIL[h];
+      const float p = exp2f(lg[k][h] - sM[h]) * sIL[h];
       a1 += p;
       a2 += p * p;
     }
-    float2* ap = isq ? &sm.acc_q[i - n_o] : &sm.acc_o[i];
-    if (first) {
-      *ap = make_float2(a1, a2);
-    } else {
-      const float2 c = *ap;
-      *ap = make_float2(c.x + a1, c.y + a2);
-    }
+    float2* ap = i >= n_o ? &sm.acc_q[i - n_o] : &sm.acc_o[i];
+    *ap = make_float2(ac[k].x + a1, ac[k].y + a2);
   }
 }
 
