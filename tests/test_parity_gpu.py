@@ -527,3 +527,41 @@ def test_constant_groups_quantize_to_scale_one():
     for mode in ("asym", "sym"):
         run_parity(MID, budget=512, steps=24, seed=15, rho=[[0.3, 0.6]], layout=2, bits=4, g=64, mode=mode,
                    check_every=24, mutate=mutate)
+
+
+@pytest.mark.parametrize("kernel", [2, 3])
+def test_cuda_graph_capture_replays_eager(kernel):
+    """arkv_decode_step never syncs and passes its per-step plans (tailor jobs, HH windows,
+    persistent ranges) as kernel parameters, so a sequence of decode steps — tailors
+    included — can be captured into one CUDA graph.  Replaying it once on an identically
+    prefilled cache gives bit-identical outputs, token states, codes and scales to eager
+    execution."""
+    sh = Shape(batch=1, n_layers=2, n_q_heads=8, n_kv_heads=2, head_dim=128, prompt_len=1024, window=32)
+    steps = 48
+    ins = [[t.cuda() for t in decode_inputs(sh, s, seed=9)] for s in range(steps)]
+    qw, k, v = prefill_inputs(sh, seed=9)
+    caches = []
+    for _ in range(2):
+        gpu, _, _ = make_pair(sh, budget=256, steps=steps, layout=2, decode_kernel=kernel)
+        gpu.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda(), rho_override=[[0.7, 0.3]])
+        caches.append(gpu)
+    torch.cuda.synchronize()
+    eager = [caches[0].arkv_decode_step(q, kn, vn) for q, kn, vn in ins]
+    outs = [torch.empty_like(o) for o in eager]
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for (q, kn, vn), o in zip(ins, outs):
+            caches[1].arkv_decode_step(q, kn, vn, out=o, stream=torch.cuda.current_stream())
+    graph.replay()
+    torch.cuda.synchronize()
+    caches[0].arkv_check()
+    caches[1].arkv_check()
+    assert sum(1 for o in outs if torch.count_nonzero(o) > 0) == steps
+    for s in range(steps):
+        assert torch.equal(eager[s], outs[s]), f"step {s}"
+    for l in range(sh.n_layers):
+        for h in range(sh.n_kv_heads):
+            a, b = caches[0].arkv_export_unit(0, l, h), caches[1].arkv_export_unit(0, l, h)
+            for key in ("state", "o_k", "o_v", "q_k", "q_v", "k_scale", "k_zero", "v_scale", "v_zero"):
+                np.testing.assert_array_equal(a[key], b[key], err_msg=f"{key} layer {l} head {h}")
+            assert (a["state"] == 2).any() and (a["state"] == 3).any()  # tailors ran inside the graph
