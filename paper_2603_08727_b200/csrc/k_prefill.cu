@@ -360,14 +360,25 @@ static int launch_passes(const Geom& g, const uint16_t* q_win, const uint16_t* k
 }
 
 bool prefill_tc_available(const Geom& g);  // k_prefill_tc.cu
+int launch_prefill_ws(const Geom& g, const uint16_t* q_win, const uint16_t* k, int P, float2* partials, int n_chunks1,
+                      float2* acc_pf, int num_sms, cudaStream_t s);  // k_prefill_ws.cu
 int launch_prefill_tc(const Geom& g, const uint16_t* q_win, const uint16_t* k, int P, float2* partials, int n_chunks1,
                       float2* acc_pf, cudaStream_t s);
 
 int launch_prefill_begin(const Geom& g, const uint16_t* q_win, const uint16_t* k, int P, float* partials,
                          int n_chunks1, float2* acc_pf, double* colsum, cudaStream_t s) {
+  // ARKV_PREFILL_TC: '0' mma.sync passes, '1' the first tcgen05 kernel (one CTA per chunk),
+  // default the warp-specialised persistent tcgen05 kernel (k_prefill_ws.cu)
   const char* env = std::getenv("ARKV_PREFILL_TC");
   if (prefill_tc_available(g) && !(env && env[0] == '0')) {  // tcgen05 passes (G*W = 128, d = 128)
-    const int n = launch_prefill_tc(g, q_win, k, P, (float2*)partials, n_chunks1, acc_pf, s);
+    int n = -1;
+    if (!(env && env[0] == '1')) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      n = launch_prefill_ws(g, q_win, k, P, (float2*)partials, n_chunks1, acc_pf, sms, s);
+    }
+    if (n < 0) n = launch_prefill_tc(g, q_win, k, P, (float2*)partials, n_chunks1, acc_pf, s);
     dim3 grid((P - g.W + 255) / 256, g.batch * g.L);
     prefill_colsum_kernel<<<grid, 256, 0, s>>>(g, acc_pf, P, colsum);
     return n + 1;
