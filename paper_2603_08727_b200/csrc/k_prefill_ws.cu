@@ -62,6 +62,33 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x for x <= 0 on the FMA pipe (offloads every kPolyEvery-th exponential from the MUFU
+// unit; measured at configs[1]: every 3rd 1.00 ms, every 4th 0.92, every 8th 0.83, off
+// 0.83-0.87 ms — the epilogue is issue-bound as much as MUFU-bound, so it is off).  x = n + f with n = rint(x) (magic-number
+// rounding), f in [-1/2, 1/2]; 2^f by a degree-5 least-squares polynomial (max relative
+// error 2.3e-7 in fp32 Horner, the same order as ex2.approx); 2^n added to the exponent
+// bits.  x is clamped at -126 (the MUFU path flushes such values to 0; here they give
+// ~1e-38).
+#ifndef ARKV_PF_POLY_EVERY
+#define ARKV_PF_POLY_EVERY 0
+#endif
+constexpr int kPolyEvery = ARKV_PF_POLY_EVERY;
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: rint(x) in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  float p = 1.3266970636323094e-3f;
+  p = fmaf(p, f, 9.675459936261177e-3f);
+  p = fmaf(p, f, 5.550742521882057e-2f);
+  p = fmaf(p, f, 2.4022121727466583e-1f);
+  p = fmaf(p, f, 6.931469440460205e-1f);
+  p = fmaf(p, f, 1.0000001192092896f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+// j: the element's index in a fully unrolled loop (folds to one path per element)
+__device__ __forceinline__ float ex2_mix(float x, int j) {
+  return (kPolyEvery > 0 && (j % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1) ? ex2_poly(x) : ex2(x);
+}
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
 }
@@ -304,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               float sum = 0.f;
               if (raw) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) sum += ex2(fmaf(v[cc][j], sl2, -mn));
+                for (int j = 0; j < 32; ++j) sum += ex2_mix(fmaf(v[cc][j], sl2, -mn), j);
               } else {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) sum += ex2(v[cc][j] - mn);
@@ -327,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               // p = 2^(s - m_r) / l_r = 2^(s - (m_r + log2 l_r)): one row constant per element
-              const float p = ex2(fmaf(v[cc][j], sl2, -rc[PASS2 ? cc * 32 + j : 0]));
+              const float p = ex2_mix(fmaf(v[cc][j], sl2, -rc[PASS2 ? cc * 32 + j : 0]), j);
               a1 += p;
               a2 += p * p;
             }
