@@ -613,24 +613,17 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int off = g.mode == ARKV_QUANT_SYM ? 8 : 0;
 
-  // ---- phase 1: one warp per row ----
-  for (int j = warp; j < kTile; j += 8) {
-    const int row = tid * kTile + j;
-    if (row >= n_new) {  // rows past the segment: zeros (defined bytes; masked by the readers)
-      for (int i = lane; i < 2 * kRowH / 2; i += 32) ((uint32_t*)sm.stage[i / (kRowH / 2)][j])[i % (kRowH / 2)] = 0u;
-      if (dstQ) {
-        for (int i = lane; i < 2 * kRowC / 4; i += 32) ((uint32_t*)sm.code[i / (kRowC / 4)][j])[i % (kRowC / 4)] = 0u;
-        if (lane < NG) sm.sc[j][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      continue;
-    }
-    const int32_t sref = src[row];
-    const int kind = sref >> 28, orow = sref & 0x0FFFFFFF;
-    int pos;
-    if (kind == kSrcInput) pos = orow;
-    else if (kind == kSrcOldO) pos = om.pos_o[orow];
-    else pos = om.pos_q[orow];
-    if (lane == 0) {
+  // ---- phase 0: the source reference and position of the warp's kTile / 8 rows in two
+  // batched rounds (lane r < kTile / 8 handles row warp + 8 r) instead of two dependent
+  // loads per row inside the row loop ----
+  constexpr int RPW = kTile / 8;
+  int my_sref = 0;
+  {
+    const int row = tid * kTile + warp + 8 * lane;
+    if (lane < RPW && row < n_new) {
+      my_sref = src[row];
+      const int kind = my_sref >> 28, orow = my_sref & 0x0FFFFFFF;
+      const int pos = kind == kSrcInput ? orow : (kind == kSrcOldO ? om.pos_o[orow] : om.pos_q[orow]);
       if (dstQ) {
         nm.pos_q[row] = pos;
         nm.acc_q[row] = make_float2(0.f, 0.f);
@@ -639,6 +632,20 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
         nm.acc_o[row] = make_float2(0.f, 0.f);
       }
     }
+  }
+  // ---- phase 1: one warp per row ----
+  for (int j = warp, r = 0; j < kTile; j += 8, ++r) {
+    const int row = tid * kTile + j;
+    const int32_t sref = __shfl_sync(0xffffffffu, my_sref, r);
+    if (row >= n_new) {  // rows past the segment: zeros (defined bytes; masked by the readers)
+      for (int i = lane; i < 2 * kRowH / 2; i += 32) ((uint32_t*)sm.stage[i / (kRowH / 2)][j])[i % (kRowH / 2)] = 0u;
+      if (dstQ) {
+        for (int i = lane; i < 2 * kRowC / 4; i += 32) ((uint32_t*)sm.code[i / (kRowC / 4)][j])[i % (kRowC / 4)] = 0u;
+        if (lane < NG) sm.sc[j][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      continue;
+    }
+    const int kind = sref >> 28, orow = sref & 0x0FFFFFFF;
     const int oj = orow & 31;
     if (kind == kSrcOldQ) {
       const uint8_t* qt = q_tile_ptr((uint8_t*)oslot, g, orow >> 5);
