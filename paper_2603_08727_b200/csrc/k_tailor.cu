@@ -690,16 +690,26 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
       const uint2 raw = *(const uint2*)&sm.stage[h][j][4 * lane];
       const float xv[4] = {__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
                            __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u)};
+      const bool sym = g.mode == ARKV_QUANT_SYM;
       float mn = fminf(fminf(xv[0], xv[1]), fminf(xv[2], xv[3]));
       float mx = fmaxf(fmaxf(xv[0], xv[1]), fmaxf(xv[2], xv[3]));
-      float am = fmaxf(fmaxf(fabsf(xv[0]), fabsf(xv[1])), fmaxf(fabsf(xv[2]), fabsf(xv[3])));
+      float am = 0.f;
+      if (sym) {
+        am = fmaxf(fmaxf(fabsf(xv[0]), fabsf(xv[1])), fmaxf(fabsf(xv[2]), fabsf(xv[3])));
 #pragma unroll
-      for (int o = 1; o < LPG; o <<= 1) {
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+        for (int o = 1; o < LPG; o <<= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+      } else if (LPG == 32) {
+        // one group per warp (g = d, the paper's "per-token scale"): sm_100a's f32 warp
+        // reduction instead of five shuffle + min/max rounds (exact: min/max of the values)
+        asm("redux.sync.min.f32 %0, %0, 0xffffffff;\n" : "+f"(mn));
+        asm("redux.sync.max.f32 %0, %0, 0xffffffff;\n" : "+f"(mx));
+      } else {
+#pragma unroll
+        for (int o = 1; o < LPG; o <<= 1) {
+          mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
       }
-      const bool sym = g.mode == ARKV_QUANT_SYM;
       const bool flat = sym ? am == 0.f : mx == mn;
       const float s = flat ? 1.f : (sym ? __fdiv_rn(am, 7.f) : __fdiv_rn(__fsub_rn(mx, mn), 15.f));
       const float z = sym ? 0.f : mn;
