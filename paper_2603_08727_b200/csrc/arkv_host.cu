@@ -450,8 +450,14 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   bool fast_ok = decode_fast_available(s.g);
   c->fast = cfg->decode_kernel == 1 ? false : fast_ok;
   {
-    const char* e = std::getenv("ARKV_DECODE_PERSIST");  // measurement override for auto
-    c->persist = c->fast && (cfg->decode_kernel == 3 || (cfg->decode_kernel == 0 && e && std::atoi(e) != 0));
+    // auto (decode_kernel = 0): the persistent range-partitioned kernel when a step has many
+    // small units (>= 32 per SM: split-K would run them as ~1-split CTAs in dozens of waves;
+    // measured at configs[3], 16384 units: 35.7K vs 33.8K tok/s), else split-K (configs[1],
+    // configs[2] per GPU, configs[4] per GPU: split-K 3-12 % faster).  ARKV_DECODE_PERSIST
+    // overrides the rule (measurement).
+    const char* e = std::getenv("ARKV_DECODE_PERSIST");
+    const bool auto_persist = e ? std::atoi(e) != 0 : s.g.n_units >= 32 * c->num_sms;
+    c->persist = c->fast && (cfg->decode_kernel == 3 || (cfg->decode_kernel == 0 && auto_persist));
   }
   if ((cfg->decode_kernel == 2 || cfg->decode_kernel == 3) && !fast_ok) {
     delete c;
