@@ -48,6 +48,7 @@ class Cfg:
     gamma: float = 263.81
     stat_eps: float = 1e-30          # R6
     sm_scale: float = 0.0            # 0 -> 1/sqrt(head_dim) (R27)
+    smooth: float = 0.0              # λ of the "smoothed" scores (Alg. 1; R34, NEXT-4); 0 = off (R21)
 
     def __post_init__(self):
         if self.group_size == 0:
@@ -82,6 +83,8 @@ def validate(cfg: Cfg) -> None:
         raise ValueError("quant_mode")
     if cfg.quant_mode == "fp8" and cfg.quant_bits != 8:
         raise ValueError("fp8 codes are 8 bits")
+    if not 0.0 <= cfg.smooth < 1.0:
+        raise ValueError("smooth must lie in [0, 1)")
 
 
 # ----------------------------------------------------------------------------
@@ -273,6 +276,22 @@ def hh_scores(samples: np.ndarray, gamma: float) -> np.ndarray:
     return mu + gamma * var
 
 
+def smooth_scores(S: np.ndarray, positions: np.ndarray, prev: Dict[int, float], lam: float) -> np.ndarray:
+    """Alg. 1 P:285 ranks tokens by "smoothed" heavy-hitter scores without defining the
+    smoothing; reading R34 (NEXT-4; parity unpinned by the paper): an exponential moving
+    average across tailors, S~_j = λ·S~_j(previous tailor) + (1 − λ)·S_j for a token that
+    the previous tailor scored and kept, S~_j = S_j for a token it did not score (appended
+    since, or inside its protected window).  λ = 0 is the unsmoothed Eq. 9 score."""
+    S = np.asarray(S, dtype=np.float64)
+    if lam == 0.0:
+        return S
+    out = S.copy()
+    for i, p in enumerate(np.asarray(positions).tolist()):
+        if p in prev:
+            out[i] = lam * prev[p] + (1.0 - lam) * S[i]
+    return out
+
+
 def rank_order(scores: np.ndarray, positions: np.ndarray) -> np.ndarray:
     """Eq. 10 "Top-b" ordering with the tie-break of R22: score descending, then
     position ascending (older token first).  Returns indices best-first."""
@@ -460,6 +479,7 @@ class UnitCache:
         self.last_tailor_pos = -1          # position of the query at/after which the last tailor took effect
         self.tailors: List[Tuple[int, int, int, int]] = []
         self.margins: List[float] = []     # relative score gaps at the rank thresholds
+        self.prev_score: Dict[int, float] = {}   # R34: smoothed score of each kept token at the last tailor
 
     @property
     def n_o(self):
@@ -541,7 +561,9 @@ class UnitCache:
         elig, win = self.eligible()
         S = self.scores(rows) if scores is None else np.asarray(scores, dtype=np.float64)
         assert len(S) == len(elig)
+        S = smooth_scores(S, elig, self.prev_score, cfg.smooth)   # R34 (identity when λ = 0)
         st = plan_states(S, elig, n_oe, n_q)
+        self.prev_score = {int(p): float(x) for p, x, s_ in zip(elig, S, st) if s_ in (1, 2)}
         # score margin at the two rank thresholds (exact ties are resolved by position
         # identically on both sides; near-ties would make fp32 vs fp64 rankings differ)
         Ss = np.sort(S)[::-1]
