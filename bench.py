@@ -166,7 +166,7 @@ def run_arkv(args, wl):
     cfg = A.make_config(L, Hq, Hkv, d, batch=B, window=wl["window"], budget_tokens=budget,
                         quant_bits=wl["bits"], group_size=wl["group"], max_positions=P + total_steps + 1,
                         quant_mode={"asym": A.QUANT_ASYM, "fp8": A.QUANT_FP8}[wl["qmode"]],
-                        state_sharing=1 if args.sharing == "layer" else 0,
+                        state_sharing=1 if args.sharing == "layer" else 0, smooth=args.smooth,
                         max_prompt=P, decode_kernel=args.kernel)
     cache = A.ArkvCache(cfg, dev)
     sh = Shape(batch=B, n_layers=L, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, prompt_len=P, window=wl["window"])
@@ -345,7 +345,7 @@ def run_arkv(args, wl):
         "config": {"workload": f"{args.workload} (BASELINE.json configs[{wl['baseline_cfg']}])",
                    "layers": L, "q_heads": Hq, "kv_heads": Hkv, "head_dim": d, "batch_per_gpu": B,
                    "global_batch": B * ws, "prompt_len": P, "budget_tokens": budget, "window": wl["window"], "mode": args.mode,
-                   "state_sharing": args.sharing,
+                   "state_sharing": args.sharing, "smooth": args.smooth,
                    "quant": (f"int{wl['bits']} g{wl['group']} asym" if wl["qmode"] == "asym"
                              else f"fp8 e4m3 g{wl['group']}"), "alpha": 0.75,
                    "launch": "one arkv_decode_step per step covering all layers (layer-batched)",
@@ -508,6 +508,8 @@ def main():
                     help="arkv (stats-driven rho) or the paper's baselines: base, origin (rho=1), quant (rho=0)")
     ap.add_argument("--prompt-len", type=int, default=0, help="debug: override the workload's prompt length")
     ap.add_argument("--layers", type=int, default=0, help="debug: override the workload's layer count")
+    ap.add_argument("--smooth", type=float, default=0.0,
+                    help="lambda of the smoothed heavy-hitter scores (NEXT-4, reading R34); 0 = off")
     ap.add_argument("--sharing", default="head", choices=["head", "layer"],
                     help="token states per KV head (R20) or per layer from group-averaged scores (NEXT-3)")
     ap.add_argument("--quant", default="int4", choices=["int4", "fp8"],

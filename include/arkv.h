@@ -85,6 +85,9 @@ typedef struct arkv_config {
   int32_t state_sharing; /* 0: one token-state set per KV head (R20); 1: one per layer, from the
                             Eq. 9 score averaged across the layer's KV heads (NEXT-3;
                             all KV heads of a layer must live in this cache) */
+  float smooth;          /* λ of the "smoothed" heavy-hitter scores (Alg. 1; reading R34,
+                            NEXT-4): S~ = λ S~(previous tailor) + (1 - λ) S for tokens the previous
+                            tailor scored and kept; 0 = off (R21, default); must lie in [0, 1) */
 } arkv_config;
 
 typedef struct arkv_cache arkv_cache; /* opaque, host-side; owned by the library */

@@ -30,6 +30,7 @@ class ArkvConfig(ctypes.Structure):
         ("decode_kernel", ctypes.c_int32),
         ("alpha", ctypes.c_double), ("tau", ctypes.c_double * 3), ("gamma", ctypes.c_double),
         ("stat_eps", ctypes.c_double), ("sm_scale", ctypes.c_float), ("state_sharing", ctypes.c_int32),
+        ("smooth", ctypes.c_float),
     ]
 
 
@@ -110,7 +111,7 @@ def make_config(n_layers, n_q_heads, n_kv_heads, head_dim, batch=1, window=32, b
                 quant_bits=4, group_size=0, quant_mode=QUANT_ASYM, max_positions=4096, max_prompt=None,
                 layout=LAYOUT_AUTO, n_spare_slots=0, max_splits=0, decode_kernel=0, alpha=0.75,
                 tau=(7.774, 5.407, 5.528), gamma=263.81, stat_eps=1e-30, sm_scale=0.0,
-                state_sharing=0) -> ArkvConfig:
+                state_sharing=0, smooth=0.0) -> ArkvConfig:
     c = ArkvConfig()
     _ok(lib().arkv_config_default(ctypes.byref(c)), "arkv_config_default")
     c.n_layers, c.n_q_heads, c.n_kv_heads, c.head_dim, c.batch = n_layers, n_q_heads, n_kv_heads, head_dim, batch
@@ -120,6 +121,7 @@ def make_config(n_layers, n_q_heads, n_kv_heads, head_dim, batch=1, window=32, b
     c.layout, c.n_spare_slots, c.max_splits, c.decode_kernel = layout, n_spare_slots, max_splits, decode_kernel
     c.alpha, c.gamma, c.stat_eps, c.sm_scale = alpha, gamma, stat_eps, sm_scale
     c.state_sharing = state_sharing
+    c.smooth = smooth
     for i in range(3):
         c.tau[i] = tau[i]
     return c

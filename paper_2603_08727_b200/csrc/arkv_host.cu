@@ -32,6 +32,8 @@ struct arkv_cache {
   int8_t* st_scratch = nullptr;
   int32_t* src_scratch = nullptr;
   float* sscore = nullptr;
+  float* ssm = nullptr;
+  std::vector<int32_t> sm_thr;  // per (sequence, layer): rows with position <= this carry a smoothed score
   // layer-shared states across KV-head shards: score sums exchanged by the caller, consumed
   // by the next call that runs tailors (arkv_set_tailor_scores)
   const float* ext_scores = nullptr;
@@ -77,7 +79,7 @@ struct Sizes {
   int n_spare, jobs_per_wave, jobs_scratch, max_splits, n_chunks1;
   int64_t arena, ws;
   int64_t off_meta, off_desc, off_err;
-  int64_t w_partials, w_logits, w_st, w_sscore, w_src, w_pfp, w_accpf, w_oq, w_colsum, w_mstat, w_counters, w_plan, w_pparts;
+  int64_t w_partials, w_logits, w_st, w_sscore, w_ssm, w_src, w_pfp, w_accpf, w_oq, w_colsum, w_mstat, w_counters, w_plan, w_pparts;
 };
 
 int64_t cost_o(const arkv_config& c) { return 4LL * c.head_dim; }
@@ -108,6 +110,7 @@ arkv_status validate(const arkv_config* c) {
   if (c->layout < 0 || c->layout > 2) return ARKV_ERR_CONFIG;
   if (c->decode_kernel < 0 || c->decode_kernel > 3) return ARKV_ERR_CONFIG;
   if (c->state_sharing != 0 && c->state_sharing != 1) return ARKV_ERR_CONFIG;
+  if (!(c->smooth >= 0.f && c->smooth < 1.f)) return ARKV_ERR_CONFIG;
   // layer-shared tailors run a layer's KV heads in one wave (one spare slot each)
   if (c->state_sharing == 1 && c->n_spare_slots > 0 && c->n_spare_slots < c->n_kv_heads) return ARKV_ERR_CONFIG;
   return ARKV_OK;
@@ -128,6 +131,7 @@ Sizes compute_sizes(const arkv_config& c) {
   g.ng = g.d / g.g;
   g.mode = c.quant_mode;
   g.share = c.state_sharing;
+  g.smooth = c.smooth;
   g.layout = c.layout;
   if (g.layout == ARKV_LAYOUT_AUTO)
     g.layout = ((c.quant_bits == 4 || c.quant_mode == ARKV_QUANT_FP8) && c.head_dim % 32 == 0) ? ARKV_LAYOUT_FRAG
@@ -143,7 +147,8 @@ Sizes compute_sizes(const arkv_config& c) {
   g.max_pos = c.max_positions;
   g.n_units = g.batch * g.L * g.Hkv;
   g.slot_bytes = round_up(Bb + g.tile_o + g.tile_q, 256);
-  g.meta_bytes = round_up((int64_t)g.cap_o * 12 + (int64_t)g.cap_q * 12, 256);
+  g.meta_bytes = round_up((int64_t)g.cap_o * (c.smooth > 0.f ? 16 : 12) + (int64_t)g.cap_q * (c.smooth > 0.f ? 16 : 12),
+                          256);  // pos, acc (+ smoothed score, R34)
   g.sm_scale = c.sm_scale > 0.f ? c.sm_scale : (float)(1.0 / std::sqrt((double)g.d));
   g.gamma = (float)c.gamma;
 
@@ -171,6 +176,8 @@ Sizes compute_sizes(const arkv_config& c) {
   w = round_up(w + (int64_t)s.jobs_scratch * st_stride, 256);
   s.w_sscore = w;  // layer-shared scores of the eligible rows, per job
   w = round_up(w + (c.state_sharing ? (int64_t)s.jobs_scratch * st_stride * 4 : 0), 256);
+  s.w_ssm = w;  // smoothed scores of the old rows, per job (R34)
+  w = round_up(w + (c.smooth > 0.f ? (int64_t)s.jobs_scratch * st_stride * 4 : 0), 256);
   s.w_src = w;
   w = round_up(w + (int64_t)s.jobs_scratch * (g.cap_o + g.cap_q) * 4, 256);
   s.w_pfp = w;
@@ -424,6 +431,7 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   c->st_scratch = (int8_t*)(w + s.w_st);
   c->src_scratch = (int32_t*)(w + s.w_src);
   c->sscore = (float*)(w + s.w_sscore);
+  c->ssm = (float*)(w + s.w_ssm);
   c->pf_partials = (float*)(w + s.w_pfp);
   c->acc_pf = (float2*)(w + s.w_accpf);
   c->oq_tmp = (double*)(w + s.w_oq);
@@ -444,6 +452,7 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   c->n_q.assign(BL, 0);
   c->t_next.assign(BL, 0);
   c->trig.assign(BL, 0);
+  c->sm_thr.assign(BL, -1);
   c->unit_slot.resize(s.g.n_units);
   for (int u = 0; u < s.g.n_units; ++u) c->unit_slot[u] = u;
   for (int k = c->n_slots - 1; k >= s.g.n_units; --k) c->spare.push_back(k);
@@ -552,6 +561,7 @@ static arkv_status run_jobs(arkv_cache* c, std::vector<TailorJob>& jobs, const u
     }
     SharedScores shs;
     shs.sscore = c->sscore;
+    shs.ssm = c->ssm;
     shs.ext = c->ext_scores;
     shs.ext_stride = c->ext_stride;
     shs.ext_heads = c->ext_heads;
@@ -657,8 +667,11 @@ arkv_status arkv_prefill_finish(arkv_cache* c, const void* k, const void* v, int
       jb.t_next = P;
       jb.identity = tailor ? 0 : 1;
       jb.ext_row = (tailor && c->ext_scores) ? bl : -1;  // arkv_tailor_scores rows: every (b, l)
+      jb.prev_thr = -1;  // the first tailor of the sequence: no smoothed scores yet (R34)
       jobs.push_back(jb);
     }
+    // R34: the prefill tailor scored (and kept or evicted) every position < P - W
+    c->sm_thr[bl] = tailor ? P - g.W - 1 : -1;
   }
   arkv_status st = run_jobs(c, jobs, (const uint16_t*)k, (const uint16_t*)v, P, s);
   c->ext_scores = nullptr;  // consumed
@@ -897,6 +910,7 @@ arkv_status arkv_tailor_scores(arkv_cache* c, int32_t layer0, int32_t n_layers, 
           jb.n_o_old = P;
           jb.n_win_old = g.W;
           jb.ext_row = -1;
+          jb.prev_thr = -1;
           jobs.push_back(jb);
         }
       max_ne = P - g.W;
@@ -915,6 +929,7 @@ arkv_status arkv_tailor_scores(arkv_cache* c, int32_t layer0, int32_t n_layers, 
           jb.n_q_old = c->n_q[bl];
           jb.n_win_old = g.W - 1;
           jb.ext_row = -1;
+          jb.prev_thr = -1;
           jobs.push_back(jb);
         }
         max_ne = std::max(max_ne, c->n_o[bl] - (g.W - 1) + c->n_q[bl]);
@@ -987,8 +1002,10 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
           jb.t_next = t;
           jb.identity = 0;
           jb.ext_row = c->ext_scores ? n_due : -1;  // arkv_tailor_scores rows: due (b, l) in order
+          jb.prev_thr = c->sm_thr[bl];
           jobs.push_back(jb);
         }
+        c->sm_thr[bl] = t - g.W;  // this tailor scores positions <= t - W (the W newest are the window)
         c->n_o[bl] = n_o_after - 1;
         c->n_q[bl] = (int)qn;
         c->trig[bl] = trig_new;

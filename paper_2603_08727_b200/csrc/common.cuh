@@ -43,6 +43,7 @@ struct Geom {
   int64_t meta_bytes;             // per-slot metadata: pos_o, pos_q, acc_o, acc_q
   float sm_scale, gamma;
   int32_t share;                  // 1: layer-shared token states (NEXT-3)
+  float smooth;                   // λ of the smoothed scores (R34, NEXT-4); 0 = off
 };
 
 struct __align__(32) UnitDesc {
@@ -68,6 +69,8 @@ struct SlotMeta {
   int32_t* pos_q;
   float2* acc_o;
   float2* acc_q;
+  float* sp_o;  // smoothed score of each row at the tailor that wrote it (smooth > 0 only)
+  float* sp_q;
 };
 __host__ __device__ inline SlotMeta slot_meta(uint8_t* meta_base, const Geom& g, int slot) {
   uint8_t* m = meta_base + (int64_t)slot * g.meta_bytes;
@@ -76,6 +79,8 @@ __host__ __device__ inline SlotMeta slot_meta(uint8_t* meta_base, const Geom& g,
   s.pos_q = s.pos_o + g.cap_o;
   s.acc_o = (float2*)(s.pos_q + g.cap_q);
   s.acc_q = s.acc_o + g.cap_o;
+  s.sp_o = (float*)(s.acc_q + g.cap_q);
+  s.sp_q = s.sp_o + g.cap_o;
   return s;
 }
 

@@ -33,10 +33,13 @@ __device__ __forceinline__ uint64_t hh_key(float2 acc, int pos, float invN, floa
 struct RowView {
   const float2* acc_o;
   const float2* acc_q;
+  const float* sp_o;  // smoothed scores of the previous tailor (R34; smooth > 0, decode only)
+  const float* sp_q;
   const int32_t* pos_o;
   const int32_t* pos_q;
   int n_elig_o, n_q;
   bool prefill;
+  __device__ float sp(int i) const { return i < n_elig_o ? sp_o[i] : sp_q[i - n_elig_o]; }
   __device__ void get(int i, float2& a, int& p) const {
     if (i < n_elig_o) {
       a = acc_o[i];
@@ -68,6 +71,7 @@ __device__ __forceinline__ RowView make_rowview(const Geom& g, const TailorJob& 
     rv.pos_o = nullptr;
     rv.acc_q = nullptr;
     rv.pos_q = nullptr;
+    rv.sp_o = rv.sp_q = nullptr;
     rv.prefill = true;
   } else {
     SlotMeta sm = slot_meta(meta, g, jb.old_slot);
@@ -75,6 +79,8 @@ __device__ __forceinline__ RowView make_rowview(const Geom& g, const TailorJob& 
     rv.acc_q = sm.acc_q;
     rv.pos_o = sm.pos_o;
     rv.pos_q = sm.pos_q;
+    rv.sp_o = sm.sp_o;
+    rv.sp_q = sm.sp_q;
     rv.prefill = false;
   }
   rv.n_elig_o = jb.n_o_old - jb.n_win_old;
@@ -121,7 +127,7 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
                                                              int8_t* __restrict__ st_scratch, int st_stride,
                                                              const float* __restrict__ sscore,
                                                              const float* __restrict__ ext, int64_t ext_stride,
-                                                             int ext_heads) {
+                                                             int ext_heads, float* __restrict__ ssm) {
   __shared__ uint32_t hist[2][256];
   __shared__ uint64_t sh_prefix[2];
   __shared__ uint32_t sh_rem[2];
@@ -154,11 +160,26 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
       ssum = sscore + (int64_t)(blockIdx.x / g.Hkv) * st_stride;
     }
   }
-  auto key_of = [&](int i) -> uint64_t {
+  // R34 (NEXT-4): tokens the previous tailor scored and kept (position <= prev_thr) rank by
+  // S~ = λ S~_prev + (1 - λ) S; the others by S
+  const float lam = g.smooth;
+  auto score_of = [&](int i, int& p) -> float {
     float2 a;
-    int p;
     rv.get(i, a, p);
-    return g.share ? score_key(__fdiv_rn(__ldcg(ssum + i), nheads), p) : hh_key(a, p, invN, gamma);
+    float S = g.share ? __fdiv_rn(__ldcg(ssum + i), nheads) : hh_score(a, invN, gamma);
+    if (lam > 0.f && p <= jb.prev_thr) S = __fadd_rn(__fmul_rn(lam, rv.sp(i)), __fmul_rn(__fsub_rn(1.f, lam), S));
+    return S;
+  };
+  auto key_of = [&](int i) -> uint64_t {
+    if (lam == 0.f && !g.share) {
+      float2 a;
+      int p;
+      rv.get(i, a, p);
+      return hh_key(a, p, invN, gamma);
+    }
+    int p;
+    const float S = score_of(i, p);
+    return score_key(S, p);
   };
 
   const uint32_t kk[2] = {(uint32_t)jb.n_oe, (uint32_t)(jb.n_oe + jb.n_q_new)};
@@ -220,8 +241,17 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
   // thresholds: k-th largest key (k == 0 -> nothing selected)
   const uint64_t T1 = kk[0] == 0 ? ~0ull : sh_prefix[0];
   const uint64_t T2 = kk[1] == 0 ? ~0ull : sh_prefix[1];
+  float* sso = ssm ? ssm + (int64_t)blockIdx.x * st_stride : nullptr;
   for (int i = threadIdx.x; i < n_e; i += blockDim.x) {
-    const uint64_t key = key_of(i);
+    uint64_t key;
+    if (sso) {  // the move kernel stores every kept row's smoothed score in the new slot
+      int p;
+      const float S = score_of(i, p);
+      key = score_key(S, p);
+      sso[i < n_elig_o ? i : q_off + (i - n_elig_o)] = S;
+    } else {
+      key = key_of(i);
+    }
     int8_t s = key >= T1 ? 1 : (key >= T2 ? 2 : 3);
     if (i < n_elig_o)
       st[i] = s;
@@ -378,7 +408,8 @@ template <int VPL, int DC>  // values per lane = ceil(d / 32); DC = compile-time
 __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs jobs, uint8_t* slots, uint8_t* meta,
                                                           const uint16_t* __restrict__ pk,
                                                           const uint16_t* __restrict__ pv, int P,
-                                                          const int32_t* __restrict__ src_scratch, int src_stride) {
+                                                          const int32_t* __restrict__ src_scratch, int src_stride,
+                                                          const float* __restrict__ ssm) {
   extern __shared__ __align__(16) uint8_t tile[];
   griddep_wait();
   Geom g = g_in;
@@ -429,6 +460,11 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
       } else {
         nm.pos_o[row] = pos;
         nm.acc_o[row] = make_float2(0.f, 0.f);
+      }
+      if (ssm) {  // R34: the row's smoothed score at this tailor (read only if it was eligible)
+        const int st_stride = max(g.max_pos, g.cap_o) + g.cap_q;
+        const float sc = ssm[(int64_t)blockIdx.y * st_stride + (kind == kSrcOldQ ? st_stride - g.cap_q + orow : orow)];
+        (dstQ ? nm.sp_q : nm.sp_o)[row] = sc;
       }
     }
     const uint8_t* qt = nullptr;
@@ -583,7 +619,7 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
                                                                uint8_t* meta, const uint16_t* __restrict__ pk,
                                                                const uint16_t* __restrict__ pv, int P,
                                                                const int32_t* __restrict__ src_scratch,
-                                                               int src_stride) {
+                                                               int src_stride, const float* __restrict__ ssm) {
   using namespace mvf;
   __shared__ __align__(16) Smem sm;
   griddep_wait();
@@ -630,6 +666,11 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
       } else {
         nm.pos_o[row] = pos;
         nm.acc_o[row] = make_float2(0.f, 0.f);
+      }
+      if (ssm) {  // R34: the row's smoothed score at this tailor (read only if it was eligible)
+        const int st_stride = max(g.max_pos, g.cap_o) + g.cap_q;
+        const float sc = ssm[(int64_t)blockIdx.y * st_stride + (kind == kSrcOldQ ? st_stride - g.cap_q + orow : orow)];
+        (dstQ ? nm.sp_q : nm.sp_o)[row] = sc;
       }
     }
   }
@@ -826,20 +867,21 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
     extra = 1;
   }
   launch_pdl(tailor_select_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, meta, acc_pf, st_scratch, st_stride,
-             (const float*)shs.sscore, shs.ext, shs.ext_stride, shs.ext_heads);
+             (const float*)shs.sscore, shs.ext, shs.ext_stride, shs.ext_heads, g.smooth > 0.f ? shs.ssm : nullptr);
   launch_pdl(tailor_scan_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, desc, (const int8_t*)st_scratch, st_stride,
              src_scratch, src_stride, err);
   dim3 grid(max_tiles, n_jobs);
+  const float* ssm = g.smooth > 0.f ? shs.ssm : nullptr;
   if (g.layout == ARKV_LAYOUT_FRAG && g.d == mvf::D && g.bits == 4 && std::getenv("ARKV_MOVE_GENERIC") == nullptr) {
     switch (g.ng) {
       case 1: launch_pdl(tailor_move_frag_kernel<1>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride); return 3 + extra;
+                         (const int32_t*)src_scratch, src_stride, ssm); return 3 + extra;
       case 2: launch_pdl(tailor_move_frag_kernel<2>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride); return 3 + extra;
+                         (const int32_t*)src_scratch, src_stride, ssm); return 3 + extra;
       case 4: launch_pdl(tailor_move_frag_kernel<4>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride); return 3 + extra;
+                         (const int32_t*)src_scratch, src_stride, ssm); return 3 + extra;
       case 8: launch_pdl(tailor_move_frag_kernel<8>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride); return 3 + extra;
+                         (const int32_t*)src_scratch, src_stride, ssm); return 3 + extra;
       default: break;
     }
   }
@@ -848,7 +890,7 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
 #define MV_LAUNCH(V, DCV)                                                                                         \
   cudaFuncSetAttribute(tailor_move_kernel<V, DCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
   launch_pdl(tailor_move_kernel<V, DCV>, grid, dim3(256), smem, s, g, jobs, slots, meta, pk, pv, P,                 \
-             (const int32_t*)src_scratch, src_stride);
+             (const int32_t*)src_scratch, src_stride, ssm);
 #define MV_CASE(V)       \
   case V:                \
     MV_LAUNCH(V, 0)      \

@@ -25,6 +25,8 @@ struct TailorJob {
   int32_t t_next;     // position of the next appended token
   int32_t identity;   // 1: no selection, every old row stays Original (prefill ingest)
   int32_t ext_row;    // layer-shared states: row of the exchanged score sums (-1: local heads only)
+  int32_t prev_thr;   // smoothed scores (R34): rows with position <= prev_thr were scored and kept
+                      // by the previous tailor (their smoothed score is in the slot meta); -1: none
 };
 struct TailorJobs {
   TailorJob j[kMaxJobs];
@@ -42,6 +44,7 @@ int launch_prefill_finish(const Geom& g, const double* colsum, int P, double* st
 // heads (sscore, written by launch_tailor_scores inside launch_tailor) or from exchanged sums
 // over every shard's heads (ext, ext_stride floats per due (sequence, layer), ext_heads heads).
 struct SharedScores {
+  float* ssm = nullptr;  // smoothed scores (R34): [job][old O rows | old Q rows], select -> move
   float* sscore = nullptr;
   const float* ext = nullptr;
   int64_t ext_stride = 0;

@@ -42,18 +42,18 @@ def _bf16_bits_to_f64(u16):
 
 
 def make_pair(sh: Shape, budget, bits=4, g=0, mode="asym", layout=0, steps=64, decode_kernel=0, max_splits=0,
-              n_spare=0, sharing="head"):
+              n_spare=0, sharing="head", smooth=0.0):
     from paper_2603_08727_b200 import arkv as A
     cfg = A.make_config(sh.n_layers, sh.n_q_heads, sh.n_kv_heads, sh.head_dim, batch=sh.batch, window=sh.window,
                         budget_tokens=budget, quant_bits=bits, group_size=g,
                         quant_mode={"asym": A.QUANT_ASYM, "sym": A.QUANT_SYM, "fp8": A.QUANT_FP8}[mode],
                         max_positions=sh.prompt_len + steps + 1, max_prompt=sh.prompt_len, layout=layout,
                         decode_kernel=decode_kernel, max_splits=max_splits, n_spare_slots=n_spare,
-                        state_sharing=1 if sharing == "layer" else 0)
+                        state_sharing=1 if sharing == "layer" else 0, smooth=smooth)
     gpu = A.ArkvCache(cfg, "cuda")
     ocfg = O.Cfg(n_layers=sh.n_layers, n_q_heads=sh.n_q_heads, n_kv_heads=sh.n_kv_heads, head_dim=sh.head_dim,
                  batch=sh.batch, window=sh.window, budget_tokens=budget, quant_bits=bits, group_size=g or sh.head_dim,
-                 quant_mode=mode, state_sharing=sharing)
+                 quant_mode=mode, state_sharing=sharing, smooth=smooth)
     return gpu, O.OracleARKV(ocfg), ocfg
 
 
@@ -565,3 +565,20 @@ def test_cuda_graph_capture_replays_eager(kernel):
             for key in ("state", "o_k", "o_v", "q_k", "q_v", "k_scale", "k_zero", "v_scale", "v_zero"):
                 np.testing.assert_array_equal(a[key], b[key], err_msg=f"{key} layer {l} head {h}")
             assert (a["state"] == 2).any() and (a["state"] == 3).any()  # tailors ran inside the graph
+
+
+@pytest.mark.parametrize("lam,kernel,sharing", [(0.5, 2, "head"), (0.9, 3, "head"), (0.5, 2, "layer")])
+def test_smoothed_scores(lam, kernel, sharing):
+    """NEXT-4 (Alg. 1 P:285 "smoothed", reading R34): scores averaged across tailors.  The
+    prefill tailor and two decode tailors per unit; the decode tailors rank the tokens the
+    previous tailor kept by λ·S~_prev + (1 − λ)·S — bit-exact states, codes and scales."""
+    sh = Shape(batch=1, n_layers=2, n_q_heads=8, n_kv_heads=2, head_dim=128, prompt_len=2048, window=32)
+    r = run_parity(sh, budget=256, steps=100, seed=61, rho=[[0.7, 0.3]], layout=2, decode_kernel=kernel,
+                   check_every=25, smooth=lam, sharing=sharing)
+    assert r["tailors"] >= 3 * 2 * 2
+    # the smoothing changed decisions: the same run without it ends in other states
+    gpu0 = run_parity(sh, budget=256, steps=100, seed=61, rho=[[0.7, 0.3]], layout=2, decode_kernel=kernel,
+                      check_every=100, smooth=0.0, sharing=sharing)["gpu"]
+    diff = sum(int((r["gpu"].arkv_export_unit(0, l, h)["state"] != gpu0.arkv_export_unit(0, l, h)["state"]).sum())
+               for l in range(2) for h in range(2))
+    assert diff > 0
