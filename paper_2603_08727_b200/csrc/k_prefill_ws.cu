@@ -44,6 +44,15 @@ constexpr int kEpiWarps = ARKV_PF_EPI_WARPS;  // 4 lane quadrants x kCG column g
 constexpr int kCG = kEpiWarps / 4;
 constexpr int kCols = 128 / kCG;             // accumulator columns per epilogue warp
 static_assert(kCols == 32 || kCols == 64, "column group of 32 or 64");
+// Pass-2 epilogue split: kTG = 1 -> the kCG warp groups take alternate tiles (each warp all
+// 128 columns of its lane quadrant, no per-tile reduction or barrier); 0 -> every tile is
+// split into kCG column groups reduced through shared memory (pass 1 always: its per-row
+// running max/sum merge only once per item).  Requires kCG == kAcc.  Measured at configs[1]:
+// pass 2 409 -> 373 us (ncu), both passes 0.866 -> 0.823 ms.
+#ifndef ARKV_PF_TILE_GROUPS
+#define ARKV_PF_TILE_GROUPS 1
+#endif
+constexpr bool kTG = ARKV_PF_TILE_GROUPS != 0;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 
 struct __align__(8) Ctl {
@@ -51,7 +60,7 @@ struct __align__(8) Ctl {
   uint64_t acc_full[kAcc], acc_empty[kAcc];
   uint64_t q_full, q_empty;
   uint32_t tmem;
-  float rowc[R];        // pass 2: row max + log2(row sum) of pass 1, current unit
+  alignas(16) float rowc[R];  // pass 2: row max + log2(row sum) of pass 1, current unit (float4 reads)
   float red[2][kCG][R][2];  // combine of the column groups (pass 2: double-buffered by tile)
 };
 constexpr int kSmem = 1024 /*align slack*/ + kTileB * (1 + kStages) + (int)sizeof(Ctl);
@@ -187,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < kAcc; ++i) {
       mbar_init(&ctl.acc_full[i], 1);
-      mbar_init(&ctl.acc_empty[i], kEpiWarps);
+      mbar_init(&ctl.acc_empty[i], (PASS2 && kTG) ? 4 : kEpiWarps);  // the warps that read accumulator i
     }
     mbar_init(&ctl.q_full, 1);
     mbar_init(&ctl.q_empty, 1);
@@ -268,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int etid = threadIdx.x - 64;                  // 0..32*kEpiWarps-1
     const float sl2 = g.sm_scale * 1.4426950408889634f;
     int T = 0, cur_u = -1;
-    float rc[PASS2 ? kCols : 1];  // pass 2: this warp's columns' row constants (registers)
+    float rc[PASS2 && !kTG ? kCols : 1];  // pass 2, column groups: this warp's row constants
     for (int i = i0; i < i1; ++i) {
       int u, c0, c1, nt;
       w.item(i, u, c0, c1, nt);
@@ -288,29 +297,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kEpiWarps) : "memory");
 #pragma unroll
-        for (int j = 0; j < (PASS2 ? kCols : 1); ++j) rc[j] = ctl.rowc[half * kCols + j];
+        for (int j = 0; j < (PASS2 && !kTG ? kCols : 1); ++j) rc[j] = ctl.rowc[half * kCols + j];
       }
       cur_u = u;
       float run_m = -INFINITY, run_l = 0.f;
       const int qp = P - g.W + (my_lane % g.W);  // pass 1: query position of row my_lane = h*W + i
       for (int t = 0; t < nt; ++t, ++T) {
+        // tile groups (kTG): group `half` takes the tiles T = half (mod kCG), all 128 columns
+        // of its lane quadrant — no cross-warp reduction, no per-tile barrier
+        if (PASS2 && kTG && (T % kCG) != half) continue;
         const int ac = T % kAcc;
         mbar_wait(&ctl.acc_full[ac], (T / kAcc) & 1);
         __syncwarp();
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ac * 128 + half * kCols);
+        constexpr int NC = (PASS2 && kTG) ? 128 : kCols;  // this warp's accumulator columns
+        const int col0 = (PASS2 && kTG) ? 0 : half * kCols;
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ac * 128 + col0);
         const int kbase = c0 + t * NK;
         if (!PASS2) {
-          float v[kCols / 32][32];
+          // one 32-column chunk in registers at a time; the accumulator is released once
+          // its last chunk has been read
+          float v[1][32];
 #pragma unroll
-          for (int cc = 0; cc < kCols / 32; ++cc) tmem_ld32(taddr + cc * 32, v[cc]);
-          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl.acc_empty[ac]);  // accumulator copied to registers
-#pragma unroll
-          for (int cc = 0; cc < kCols / 32; ++cc) {
+          for (int cc0 = 0; cc0 < NC / 32; ++cc0) {
+            tmem_ld32(taddr + cc0 * 32, v[0]);
+            if (cc0 == NC / 32 - 1) {
+              asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&ctl.acc_empty[ac]);
+            }
+            const int cc = 0;
             float mx = -INFINITY;
-            const int key0 = kbase + half * kCols + cc * 32;
+            const int key0 = kbase + col0 + cc0 * 32;
             bool raw = false;
             if (key0 + 31 < c1 && key0 + 31 <= P - g.W) {  // no key masked (all but the last tiles)
               // max on the raw logits: x -> x * sl2 (sl2 > 0) is monotone, and so is rounding
@@ -342,36 +360,63 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           const int key = kbase + my_lane;
-          float v[kCols / 32][32];
-#pragma unroll
-          for (int cc = 0; cc < kCols / 32; ++cc) tmem_ld32(taddr + cc * 32, v[cc]);
-          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl.acc_empty[ac]);
           float a1 = 0.f, a2 = 0.f;
+          if (kTG) {
+            // 4 x 32 columns, each chunk processed as soon as it is in registers; the row
+            // constants come from shared memory (broadcast float4 reads)
 #pragma unroll
-          for (int cc = 0; cc < kCols / 32; ++cc)
+            for (int cc = 0; cc < NC / 32; ++cc) {
+              float v[32];
+              tmem_ld32(taddr + cc * 32, v);
+              if (cc == NC / 32 - 1) {
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ctl.acc_empty[ac]);
+              }
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              // p = 2^(s - m_r) / l_r = 2^(s - (m_r + log2 l_r)): one row constant per element
-              const float p = ex2_mix(fmaf(v[cc][j], sl2, -rc[PASS2 ? cc * 32 + j : 0]), j);
-              a1 += p;
-              a2 += p * p;
+              for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 r4 = *(const float4*)&ctl.rowc[cc * 32 + 4 * j4];
+                const float rr[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float p = ex2_mix(fmaf(v[4 * j4 + e], sl2, -rr[e]), 4 * j4 + e);
+                  a1 += p;
+                  a2 += p * p;
+                }
+              }
             }
-          // the quadrant's kCG warps hold the same keys: one barrier per tile (the buffer
-          // is reused two tiles later, behind the next tile's barrier)
-          float(&rd)[kCG][R][2] = ctl.red[T & 1];
-          rd[half][my_lane][0] = a1;
-          rd[half][my_lane][1] = a2;
-          asm volatile("bar.sync %0, %1;\n" ::"r"(2 + quad), "n"(32 * kCG) : "memory");
-          if (half == 0 && key < c1) {
-            float s1 = rd[0][my_lane][0], s2 = rd[0][my_lane][1];
+            if (key < c1) acc_pf[(int64_t)u * g.max_pos + key] = make_float2(a1, a2);
+          } else {
+            float v[NC / 32][32];
 #pragma unroll
-            for (int cg = 1; cg < kCG; ++cg) {
-              s1 += rd[cg][my_lane][0];
-              s2 += rd[cg][my_lane][1];
+            for (int cc = 0; cc < NC / 32; ++cc) tmem_ld32(taddr + cc * 32, v[cc]);
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ctl.acc_empty[ac]);
+#pragma unroll
+            for (int cc = 0; cc < NC / 32; ++cc)
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                // p = 2^(s - m_r) / l_r = 2^(s - (m_r + log2 l_r)): one row constant per element
+                const float p = ex2_mix(fmaf(v[cc][j], sl2, -rc[PASS2 && !kTG ? cc * 32 + j : 0]), j);
+                a1 += p;
+                a2 += p * p;
+              }
+            // the quadrant's kCG warps hold the same keys: one barrier per tile (the buffer
+            // is reused two tiles later, behind the next tile's barrier)
+            float(&rd)[kCG][R][2] = ctl.red[T & 1];
+            rd[half][my_lane][0] = a1;
+            rd[half][my_lane][1] = a2;
+            asm volatile("bar.sync %0, %1;\n" ::"r"(2 + quad), "n"(32 * kCG) : "memory");
+            if (half == 0 && key < c1) {
+              float s1 = rd[0][my_lane][0], s2 = rd[0][my_lane][1];
+#pragma unroll
+              for (int cg = 1; cg < kCG; ++cg) {
+                s1 += rd[cg][my_lane][0];
+                s2 += rd[cg][my_lane][1];
+              }
+              acc_pf[(int64_t)u * g.max_pos + key] = make_float2(s1, s2);
             }
-            acc_pf[(int64_t)u * g.max_pos + key] = make_float2(s1, s2);
           }
         }
       }
