@@ -64,6 +64,22 @@ def test_config_validation():
     a8, _ = A.arkv_cache_bytes(A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, max_positions=128,
                                              quant_bits=8, quant_mode=A.QUANT_FP8))
     assert a8 > 0
+    for lam in (-0.1, 1.0, 1.5):        # smoothed scores (R34): lambda in [0, 1)
+        with pytest.raises(A.ArkvError):
+            A.arkv_cache_bytes(A.make_config(1, 4, 2, 16, window=8, budget_tokens=32, smooth=lam))
+
+
+def test_smoothing_storage():
+    """R34 keeps one fp32 smoothed score per cached row (slot meta) and one per old row of a
+    tailor wave (workspace) — only when smoothing is on."""
+    kw = dict(window=32, budget_tokens=2048, max_positions=8192 + 64, max_prompt=8192)
+    a0, w0 = A.arkv_cache_bytes(A.make_config(4, 32, 8, 128, **kw))
+    a1, w1 = A.arkv_cache_bytes(A.make_config(4, 32, 8, 128, smooth=0.5, **kw))
+    assert a1 > a0 and w1 > w0
+    slots = 4 * 8 + 8                   # units + default spares (batch x H_kv)
+    cap_o = (2048 + 1 + 31) // 32 * 32
+    assert a1 - a0 >= slots * cap_o * 4  # at least 4 B per Original row slot
+    assert a1 - a0 < 0.05 * a0           # a few percent of the arena
 
 
 def test_arena_respects_budget():
