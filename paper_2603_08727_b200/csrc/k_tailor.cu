@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
     const uint32_t rem_in[2] = {sh_rem[0], sh_rem[1]};
     __syncthreads();
     const int sh = pass * 8;
+#pragma unroll 4
     for (int i = threadIdx.x; i < n_e; i += blockDim.x) {
       const uint64_t key = key_of(i);
       const uint32_t dg = (uint32_t)(key >> sh) & 0xFFu;
