@@ -567,17 +567,19 @@ def test_cuda_graph_capture_replays_eager(kernel):
             assert (a["state"] == 2).any() and (a["state"] == 3).any()  # tailors ran inside the graph
 
 
-@pytest.mark.parametrize("lam,kernel,sharing", [(0.5, 2, "head"), (0.9, 3, "head"), (0.5, 2, "layer")])
-def test_smoothed_scores(lam, kernel, sharing):
+@pytest.mark.parametrize("lam,kernel,sharing,layout", [(0.5, 2, "head", 2), (0.9, 3, "head", 2), (0.5, 2, "layer", 2),
+                                                        (0.5, 0, "head", 1)])
+def test_smoothed_scores(lam, kernel, sharing, layout):
     """NEXT-4 (Alg. 1 P:285 "smoothed", reading R34): scores averaged across tailors.  The
     prefill tailor and two decode tailors per unit; the decode tailors rank the tokens the
-    previous tailor kept by λ·S~_prev + (1 − λ)·S — bit-exact states, codes and scales."""
+    previous tailor kept by λ·S~_prev + (1 − λ)·S — bit-exact states, codes and scales.
+    Layout 1 (PLAIN) runs the generic decode and move kernels."""
     sh = Shape(batch=1, n_layers=2, n_q_heads=8, n_kv_heads=2, head_dim=128, prompt_len=2048, window=32)
-    r = run_parity(sh, budget=256, steps=100, seed=61, rho=[[0.7, 0.3]], layout=2, decode_kernel=kernel,
+    r = run_parity(sh, budget=256, steps=100, seed=61, rho=[[0.7, 0.3]], layout=layout, decode_kernel=kernel,
                    check_every=25, smooth=lam, sharing=sharing)
     assert r["tailors"] >= 3 * 2 * 2
     # the smoothing changed decisions: the same run without it ends in other states
-    gpu0 = run_parity(sh, budget=256, steps=100, seed=61, rho=[[0.7, 0.3]], layout=2, decode_kernel=kernel,
+    gpu0 = run_parity(sh, budget=256, steps=100, seed=61, rho=[[0.7, 0.3]], layout=layout, decode_kernel=kernel,
                       check_every=100, smooth=0.0, sharing=sharing)["gpu"]
     diff = sum(int((r["gpu"].arkv_export_unit(0, l, h)["state"] != gpu0.arkv_export_unit(0, l, h)["state"]).sum())
                for l in range(2) for h in range(2))
