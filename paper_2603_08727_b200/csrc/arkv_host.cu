@@ -238,8 +238,9 @@ bool check_cuda(cudaError_t e) {
 extern "C" {
 
 const char* arkv_version(void) {
-  return "arkv 0.2 sm_100a layouts=plain,frag decode=generic,mma-sync-split,mma-sync-persistent "
-         "prefill=tcgen05,mma-sync";
+  return "arkv 0.3 sm_100a layouts=plain,frag decode=generic,mma-sync-split,mma-sync-persistent "
+         "prefill=tcgen05-tma-ws,tcgen05,mma-sync quant=int2/4/8,fp8-e4m3 states=per-head,layer-shared "
+         "scores=eq9,smoothed";
 }
 
 const char* arkv_status_string(arkv_status s) {
