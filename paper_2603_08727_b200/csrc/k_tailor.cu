@@ -764,9 +764,10 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float num = sym ? xv[e] : __fsub_rn(xv[e], mn);
-        float q = __fmul_rn(num, r);
-        if (tiny || fabsf(q - floorf(q) - 0.5f) < 1e-5f) q = __fdiv_rn(num, s);
-        int c = __float2int_rn(q);
+        const float q = __fmul_rn(num, r);
+        const float qr = rintf(q);
+        // within 1e-5 of a half-integer <=> more than 0.5 - 1e-5 from the nearest integer
+        int c = (tiny || fabsf(q - qr) > 0.5f - 1e-5f) ? __float2int_rn(__fdiv_rn(num, s)) : (int)qr;
         c = flat ? 0 : (sym ? max(-7, min(7, c)) : max(0, min(15, c)));
         word |= (uint32_t)((c + off) & 0xFF) << (8 * e);
       }
