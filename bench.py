@@ -132,7 +132,6 @@ def unit_counts_summary(cache, wl):
 
 
 def cache_bytes_per_step(cache, wl, n_o, n_q):
-    from oracle import Cfg  # noqa: F401  (not used: bytes follow the C ABI's cost model below)
     d, G, Hkv = wl["head_dim"], wl["n_q_heads"] // wl["n_kv_heads"], wl["n_kv_heads"]
     co = 4 * d
     cq = 2 * (d * wl["bits"] // 8 + 8 * (d // wl["group"]))

@@ -233,10 +233,10 @@ def prefill_needs_tailor(P: int, cfg: Cfg) -> bool:
 
 
 def decode_needs_tailor(n_o: int, n_q: int, cfg: Cfg) -> bool:
-    """R12: after the append, tailor iff the unit exceeds its budget, U > B_bytes
-    (Eq. 1 holds with ≤ at every attention step).  Parity unpinned: "reaches the limit"
-    (P:250) does not fix > versus >=."""
-    return usage_bytes(cfg, n_o, n_q) > budget_bytes(cfg)
+    """R12: after the append, tailor iff the unit has reached its budget, U >= B_bytes
+    ("triggered when the KV cache reaches the limit"; "true iff usage
+    >= budget.total", with its boundary case usage 512.0 of 512 -> true)."""
+    return usage_bytes(cfg, n_o, n_q) >= budget_bytes(cfg)
 
 
 def schedule(P: int, n_steps: int, rho: float, cfg: Cfg):
@@ -477,6 +477,8 @@ class UnitCache:
         self.n_pos = 0                     # positions seen so far
         self.history: List[Tuple[int, np.ndarray, np.ndarray]] = []   # (query pos, key positions, probs [G][n])
         self.last_tailor_pos = -1          # position of the query at/after which the last tailor took effect
+        self.q0 = 0                        # first query position on the current cache (R19): the
+                                           # first decode call after the prompt, or the last tailor's step
         self.tailors: List[Tuple[int, int, int, int]] = []
         self.margins: List[float] = []     # relative score gaps at the rank thresholds
         self.prev_score: Dict[int, float] = {}   # R34: smoothed score of each kept token at the last tailor
@@ -511,6 +513,7 @@ class UnitCache:
         self.o_k = np.asarray(k, dtype=np.float64).copy()
         self.o_v = np.asarray(v, dtype=np.float64).copy()
         self.n_pos = P
+        self.q0 = P          # the prompt's own queries are not samples of decode tailors (R19)
 
     def keys_values(self):
         """Dequantized view of O ∪ Q (Alg. 1 'Reconstruction'), by state
@@ -539,6 +542,8 @@ class UnitCache:
         """Eq. 9 scores of the eligible tokens (ascending positions) from the Eq. 2 window
         rows: list of (key positions [n], probs [r][n]) (R19)."""
         elig, _ = self.eligible()
+        if not rows:         # no query has run on the current cache (W = 1 edge case): S = 0
+            return np.zeros(len(elig))
         blocks = []
         for kpos, pr in rows:
             col = {int(p): i for i, p in enumerate(np.asarray(kpos).tolist())}
@@ -615,6 +620,7 @@ class UnitCache:
         assert self.usage() <= budget_bytes(cfg) - W * cost_orig(cfg)
         self.tailors.append((tailor_pos, self.n_o, self.n_q, K - W - n_oe - n_q))
         self.last_tailor_pos = tailor_pos
+        self.q0 = tailor_pos     # the tailor step's own query runs after it (R13)
         self.history = []
 
     def export(self):
@@ -715,10 +721,12 @@ class OracleARKV:
                     t = u.n_pos
                     u.append(t, k[b, li, kvh], v[b, li, kvh])
                     if decode_needs_tailor(u.n_o, u.n_q, cfg):
-                        hist = u.history[-W:]
-                        assert len(hist) == W and [h[0] for h in hist] == list(range(t - W, t)), \
-                            "tailor window must be the last W queries"
-                        assert hist[0][0] >= u.last_tailor_pos, "window rows must postdate the previous tailor (R14)"
+                        # R19: the last W queries before the tailor that ran on the current
+                        # cache, i.e. positions max(t - W, q0) .. t - 1 (fewer than W only for
+                        # the first tailor after the prompt)
+                        hist = [h for h in u.history[-W:] if h[0] >= u.q0]
+                        assert [h[0] for h in hist] == list(range(max(t - W, u.q0), t)), \
+                            "tailor window must be the last W queries on the current cache"
                         rows[kvh] = [(h[1], h[2]) for h in hist]
                 if rows:
                     assert len(rows) == cfg.n_kv_heads   # counts are identical across KV heads (R15)

@@ -62,6 +62,8 @@ struct arkv_cache {
   // host mirrors
   std::vector<double> rho;
   std::vector<int> n_o, n_q, t_next, trig;  // per (b, l)
+  std::vector<int> q0;  // per (b, l): first query position on the current cache (the first decode
+                        // call after the prompt, or the step of the last decode tailor; R19)
   std::vector<int> unit_slot;               // per unit
   std::vector<int> spare;
   bool prefilled = false;
@@ -212,13 +214,18 @@ void tailor_counts(const Geom& g, double alpha, int64_t K, double rho, int64_t* 
   *n_oe = o;
   *n_q = q;
 }
-// Appends after which the unit first exceeds B_bytes (R12): the next tailor fires
-// at (position of the last counted token) + this.
+// Appends after which the unit first reaches B_bytes, U >= B_bytes (R12; "reaches
+// the limit"): the next tailor fires at (position of the last counted token) +
+// this.  After any tailor or an untailored prompt U <= B_bytes - W*C_o (R14), so this is >= W.
 int64_t appends_to_trigger(const Geom& g, int64_t n_o, int64_t n_q) {
   const int64_t Bb = (int64_t)g.B * g.cost_o;
   const int64_t U = n_o * g.cost_o + n_q * g.cost_q;
-  return (Bb - U) / g.cost_o + 1;
+  return std::max<int64_t>(1, (Bb - U + g.cost_o - 1) / g.cost_o);
 }
+
+// First position whose query is an Eq. 9 sample of the tailor at `trig` (R19): the last W
+// queries before it, but only those that ran on the current cache (from q0 on).
+int acc0_of(const Geom& g, int64_t trig, int64_t q0) { return (int)std::max<int64_t>(trig - g.W, q0); }
 
 // ARKV_DEBUG_SYNC=1: synchronize after every launch group and name the failing one.
 void debug_sync(cudaStream_t s, const char* what) {
@@ -453,6 +460,7 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   c->n_q.assign(BL, 0);
   c->t_next.assign(BL, 0);
   c->trig.assign(BL, 0);
+  c->q0.assign(BL, 0);
   c->sm_thr.assign(BL, -1);
   c->unit_slot.resize(s.g.n_units);
   for (int u = 0; u < s.g.n_units; ++u) c->unit_slot[u] = u;
@@ -654,6 +662,7 @@ arkv_status arkv_prefill_finish(arkv_cache* c, const void* k, const void* v, int
     c->n_q[bl] = (int)q;
     c->t_next[bl] = P;
     c->trig[bl] = (int)((P - 1) + appends_to_trigger(g, n_o, q));
+    c->q0[bl] = P;  // the prompt's queries are not Eq. 9 samples of decode tailors (R19)
     for (int kvh = 0; kvh < g.Hkv; ++kvh) {
       TailorJob jb{};
       jb.unit = bl * g.Hkv + kvh;
@@ -665,6 +674,8 @@ arkv_status arkv_prefill_finish(arkv_cache* c, const void* k, const void* v, int
       jb.n_oe = (int)oe;
       jb.n_q_new = (int)q;
       jb.trig_new = c->trig[bl];
+      jb.acc0_new = acc0_of(g, c->trig[bl], P);
+      jb.n_rows = g.W;  // the prompt's last W queries (Eq. 2)
       jb.t_next = P;
       jb.identity = tailor ? 0 : 1;
       jb.ext_row = (tailor && c->ext_scores) ? bl : -1;  // arkv_tailor_scores rows: every (b, l)
@@ -910,6 +921,7 @@ arkv_status arkv_tailor_scores(arkv_cache* c, int32_t layer0, int32_t n_layers, 
           jb.old_slot = -1;
           jb.n_o_old = P;
           jb.n_win_old = g.W;
+          jb.n_rows = g.W;
           jb.ext_row = -1;
           jb.prev_thr = -1;
           jobs.push_back(jb);
@@ -929,6 +941,7 @@ arkv_status arkv_tailor_scores(arkv_cache* c, int32_t layer0, int32_t n_layers, 
           jb.n_o_old = c->n_o[bl];
           jb.n_q_old = c->n_q[bl];
           jb.n_win_old = g.W - 1;
+          jb.n_rows = c->t_next[bl] - acc0_of(g, c->t_next[bl], c->q0[bl]);
           jb.ext_row = -1;
           jb.prev_thr = -1;
           jobs.push_back(jb);
@@ -1000,6 +1013,8 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
           jb.n_oe = (int)oe;
           jb.n_q_new = (int)qn;
           jb.trig_new = trig_new;
+          jb.acc0_new = acc0_of(g, trig_new, t);
+          jb.n_rows = t - acc0_of(g, t, c->q0[bl]);
           jb.t_next = t;
           jb.identity = 0;
           jb.ext_row = c->ext_scores ? n_due : -1;  // arkv_tailor_scores rows: due (b, l) in order
@@ -1010,15 +1025,17 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
         c->n_o[bl] = n_o_after - 1;
         c->n_q[bl] = (int)qn;
         c->trig[bl] = trig_new;
+        c->q0[bl] = t;  // this step's query runs after the tailor (R13)
         ++n_due;
       }
       const int tiles = (c->n_o[bl] + 1 + kTile - 1) / kTile + (c->n_q[bl] + kTile - 1) / kTile;
       max_tiles = std::max(max_tiles, tiles);
-      if (t >= c->trig[bl] - g.W && t < c->trig[bl]) {  // HH accumulation step (R19)
+      const int acc0 = acc0_of(g, c->trig[bl], c->q0[bl]);
+      if (t >= acc0 && t < c->trig[bl]) {  // HH accumulation step (R19)
         const int rows = c->n_o[bl] + 1 + c->n_q[bl];
         acc_rows = std::max(acc_rows, rows);
         if (hh.n < kMaxHhEntries)
-          hh.e[hh.n++] = make_int4(b * n_layers + (l - layer0), rows, t == c->trig[bl] - g.W ? 1 : 0, c->n_q[bl]);
+          hh.e[hh.n++] = make_int4(b * n_layers + (l - layer0), rows, t == acc0 ? 1 : 0, c->n_q[bl]);
         else
           hh_fit = false;
       }

@@ -52,7 +52,9 @@ struct __align__(32) UnitDesc {
   int32_t n_q;     // Quantized rows
   int32_t t_next;  // position of the next appended token
   int32_t trig;    // position of the next tailor (R12, R15)
-  int32_t pad0, pad1, pad2;
+  int32_t acc0;    // first position whose query is an Eq. 9 sample of that tailor (R19):
+                   // max(trig - W, first query on the current cache)
+  int32_t pad1, pad2;
 };
 
 // ---------------------------------------------------------------------------------

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(128) decode_split_generic(DecodeArgs a) {
   uint8_t* slot = a.slots + (int64_t)dsc.slot * g.slot_bytes;
   const SlotMeta sm = slot_meta(a.meta, g, dsc.slot);
   const int n_o = dsc.n_o, n_q = dsc.n_q, t = dsc.t_next;
-  const bool accm = (t >= dsc.trig - g.W) && (t < dsc.trig);
+  const bool accm = (t >= dsc.acc0) && (t < dsc.trig);
   const int tiles_o = (n_o + 1 + kTile - 1) / kTile;
   const int tiles_q = (n_q + kTile - 1) / kTile;
   const int S = a.n_splits, s = blockIdx.x;
@@ -254,8 +254,8 @@ __global__ void __launch_bounds__(256) decode_hh_acc(DecodeArgs a) {
   unit_of(a, blockIdx.y, b, li, kvh, u);
   const UnitDesc dsc = a.desc[u];
   const int t = dsc.t_next - 1;  // the step just attended
-  if (!((t >= dsc.trig - g.W) && (t < dsc.trig))) return;
-  const bool first = t == dsc.trig - g.W;
+  if (!((t >= dsc.acc0) && (t < dsc.trig))) return;
+  const bool first = t == dsc.acc0;
   const int n_rows = dsc.n_o + dsc.n_q;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_rows) return;

@@ -663,7 +663,7 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
   const UnitDesc dsc = a.desc[u];
   uint8_t* slot = a.slots + (int64_t)dsc.slot * g.slot_bytes;
   const int n_o = dsc.n_o, n_q = dsc.n_q, t_pos = dsc.t_next;
-  const bool accm = (t_pos >= dsc.trig - g.W) && (t_pos < dsc.trig);
+  const bool accm = (t_pos >= dsc.acc0) && (t_pos < dsc.trig);
   const int tiles_o = (n_o + 1 + kTile - 1) / kTile;
   const int tiles_q = (n_q + kTile - 1) / kTile;
   const int S = a.n_splits, s = blockIdx.x;
@@ -990,7 +990,7 @@ __device__ __forceinline__ void punit_fill(const DecodeArgs& a, const UnitDesc& 
   p.n_q = dsc.n_q;
   p.tiles_q = (p.n_q + kTile - 1) / kTile;
   p.items = f == 0 ? (p.n_o + kTile - 1) / kTile : (p.tiles_q + q_per - 1) / q_per;
-  p.accm = (dsc.t_next >= dsc.trig - g.W) && (dsc.t_next < dsc.trig);
+  p.accm = (dsc.t_next >= dsc.acc0) && (dsc.t_next < dsc.trig);
 }
 // Position in one phase range of a CTA: item k of unit ul.  Walks forward only (units
 // with no items of the phase are stepped over); the next unit's descriptor is prefetched
@@ -1217,7 +1217,7 @@ __global__ void __launch_bounds__(G * D) decode_persist_combine(DecodeArgs a) {
   const uint16_t* qp = a.q + (qkv * g.Hq + kvh * G) * D;
   const uint16_t* kn = a.k + (qkv * g.Hkv + kvh) * D;
   const uint16_t* vn = a.v + (qkv * g.Hkv + kvh) * D;
-  const bool accm = (dsc.t_next >= dsc.trig - g.W) && (dsc.t_next < dsc.trig);
+  const bool accm = (dsc.t_next >= dsc.acc0) && (dsc.t_next < dsc.trig);
   const int row_stride = g.cap_o + g.cap_q;
   __shared__ float s_new[G], sM[G], sIL[G];
   __shared__ float s_w[kMaxUnitParts][G];  // merge weight 2^(m - M) of each slot (0: unused)

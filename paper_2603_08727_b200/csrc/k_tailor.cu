@@ -1,6 +1,6 @@
 // k_tailor.cu — the tri-state tailor (D4-D6 / P4 of DESIGN.md §2).
 //
-//  select: heavy-hitter score S = μ + γ·max(0, acc2/N − μ²), μ = acc1/N, N = G·W
+//  select: heavy-hitter score S = μ + γ·max(0, acc2/N − μ²), μ = acc1/N, N = G·n_rows
 //          (Eq. 9; R18, R20), then a block-wide 64-bit radix select of
 //          the two rank thresholds of Eq. 10 over composite keys
 //          (S desc, position asc; R22) -> new state per old row.
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) tailor_scores_kernel(Geom g, TailorJobs j
   const int k0 = blockIdx.y * g.Hkv;
   const TailorJob& j0 = jobs.j[k0];
   const int n_e = j0.n_o_old - j0.n_win_old + j0.n_q_old;
-  const float invN = 1.0f / (float)(g.G * g.W);
+  const float invN = j0.n_rows > 0 ? 1.0f / (float)(g.G * j0.n_rows) : 0.f;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_e) return;
   float sum = 0.f;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(1024) tailor_select_kernel(Geom g, TailorJobs 
   if (jb.identity) return;
 
   const RowView rv = make_rowview(g, jb, meta, acc_pf);
-  const float invN = 1.0f / (float)(g.G * g.W);
+  const float invN = jb.n_rows > 0 ? 1.0f / (float)(g.G * jb.n_rows) : 0.f;
   const float gamma = g.gamma;
   // layer-shared states (NEXT-3): the score is the mean over the layer's KV
   // heads — the sum per row comes from tailor_scores_kernel (this cache's heads; the
@@ -357,7 +357,8 @@ __global__ void __launch_bounds__(1024) tailor_scan_kernel(Geom g, TailorJobs jo
     dd.n_q = jb.n_q_new;
     dd.t_next = jb.t_next;
     dd.trig = jb.trig_new;
-    dd.pad0 = dd.pad1 = dd.pad2 = 0;
+    dd.acc0 = jb.acc0_new;
+    dd.pad1 = dd.pad2 = 0;
     desc[jb.unit] = dd;
   }
 }

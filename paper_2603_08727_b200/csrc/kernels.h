@@ -22,6 +22,9 @@ struct TailorJob {
   int32_t n_oe;       // eligible tokens kept Original
   int32_t n_q_new;    // tokens kept Quantized
   int32_t trig_new;   // next tailor position
+  int32_t acc0_new;   // first HH accumulation position of the next tailor (R19; UnitDesc::acc0)
+  int32_t n_rows;     // Eq. 9 window queries of this tailor (prefill W; decode min(W, queries
+                      // since the previous tailor or the prompt)): N = G * n_rows samples
   int32_t t_next;     // position of the next appended token
   int32_t identity;   // 1: no selection, every old row stays Original (prefill ingest)
   int32_t ext_row;    // layer-shared states: row of the exchanged score sums (-1: local heads only)

@@ -128,3 +128,52 @@ def test_determinism():
         outs.append((np.stack(o), ora.export(0, 0, 1)["state"]))
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     np.testing.assert_array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("mode,bits,g", [("asym", 4, 8), ("sym", 8, 16), ("asym", 2, 16), ("fp8", 8, 16), ("sym", 4, 32)])
+def test_all_quantized_equals_dense_attention_over_dequantized(mode, bits, g):
+    """SURVEY §8(c) C3 pin of the Q-token attention (Alg. 1 'Reconstruction Before
+    Attention', P:294-300; P:253 'dequantized and concatenated ... attention is
+    unmodified'): with rho = 0 and alpha = 1 every non-window token is Quantized; the
+    decode output must equal textbook softmax attention over the dequantized keys/values,
+    rebuilt here element by element from the exported codes, scales and zeros (x~ = code*s
+    + z per group of g along head_dim) — independently of UnitCache.keys_values.  The
+    codes are also checked against the prompt (|x - x~| <= s/2 (+ e4m3 half-step)) so a
+    group-axis or scale/zero slip in the export fails too."""
+    d, W, P, H_q, H_kv = 32, 4, 40, 4, 2
+    sh = Shape(batch=1, n_layers=1, n_q_heads=H_q, n_kv_heads=H_kv, head_dim=d, prompt_len=P, window=W)
+    cfg = O.Cfg(n_layers=1, n_q_heads=H_q, n_kv_heads=H_kv, head_dim=d, window=W, budget_tokens=40,
+                quant_bits=bits, group_size=g, quant_mode=mode, alpha=1.0)
+    assert O.prefill_needs_tailor(P, cfg)
+    qw, k, v = prefill_inputs(sh, seed=11)
+    ora = O.OracleARKV(cfg)
+    ora.prefill(_np(qw), _np(k), _np(v), rho_override=[[0.0]])
+    q, kn, vn = decode_inputs(sh, 0, seed=11)
+    out = ora.decode_step(_np(q), _np(kn), _np(vn))
+    G = H_q // H_kv
+    for kvh in range(H_kv):
+        e = ora.export(0, 0, kvh)
+        st = e["state"]
+        assert (st[:P - W] == 2).all() and (st[P - W:] == 1).all(), "every non-window token Quantized"
+        Kt, Vt = [], []
+        for p in range(P + 1):
+            if st[p] == 1:
+                Kt.append([float(x) for x in e["o_k"][p]]); Vt.append([float(x) for x in e["o_v"][p]])
+                continue
+            kd, vd = [], []
+            for x in range(d):
+                gi = x // g
+                ck, cv = int(e["q_k"][p, x]), int(e["q_v"][p, x])
+                if mode == "fp8":
+                    ck, cv = float(O.e4m3_decode(ck)), float(O.e4m3_decode(cv))
+                kd.append(ck * float(e["k_scale"][p, gi]) + float(e["k_zero"][p, gi]))
+                vd.append(cv * float(e["v_scale"][p, gi]) + float(e["v_zero"][p, gi]))
+                for xv, xt, s in ((kd[-1], float(_np(k)[0, 0, kvh, p, x]), float(e["k_scale"][p, gi])),
+                                  (vd[-1], float(_np(v)[0, 0, kvh, p, x]), float(e["v_scale"][p, gi]))):
+                    bound = s / 2 if mode != "fp8" else abs(xt) / 16 + s * 2.0 ** -10
+                    assert abs(xv - xt) <= bound * (1 + 1e-6) + 1e-7
+            Kt.append(kd); Vt.append(vd)
+        Kt, Vt = np.array(Kt), np.array(Vt)
+        assert Kt.shape == (P + 1, d)
+        exp = _brute_attention(_np(q)[0, 0, kvh * G:(kvh + 1) * G], Kt, Vt, cfg.sm_scale)
+        np.testing.assert_allclose(out[0, 0, kvh * G:(kvh + 1) * G], exp, rtol=1e-10, atol=1e-12)

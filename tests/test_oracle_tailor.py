@@ -94,7 +94,7 @@ def test_schedule_invariants(P, steps, rho, W, dbg):
         assert n_o >= W and n_q >= 0 and n_ev >= 0
         assert O.usage_bytes(cfg, n_o, n_q) <= Bb - W * Co
         if last is not None:
-            assert s - last >= W + 1
+            assert s - last >= W      # U_after <= B_bytes - W*C_o (R14) and U >= B_bytes fires (R12)
         last = s
     # replay: usage <= budget at every attention
     n_o, n_q = (ev[0][1], ev[0][2]) if ev and ev[0][0] == -1 else (P, 0)
@@ -113,9 +113,10 @@ def test_schedule_toy_hand_derived():
     prefill K=64 -> n_e=56, b=42; rho=1: n_oe=min(24,42,16)=16, n_q=min(26,(2048-32*64)//32=0)
     -> (24, 0, 40).  rho=0.5: n_oe=12, n_q=min(30, 256//32=8)=8 -> (20, 8, 36).
     rho=0.25: n_oe=6, n_q=min(36, 640//32=20)=20 -> (14, 20, 30).  Decode: rho=1, usage
-    24*64 -> exceeds 2048 after 9 appends (step index 8): K=33, n_e=25, b=18, n_oe=16 -> (24, 0, 9)."""
+    24*64 = 1536 reaches 2048 after 8 appends (0-based step index 7): K=32, n_e=24, b=18,
+    n_oe=16 -> (24, 0, 8) (tests/test_schedule_appendix.py)."""
     cfg = toy_cfg()
-    assert O.schedule(64, 16, 1.0, cfg) == [(-1, 24, 0, 40), (8, 24, 0, 9)]
+    assert O.schedule(64, 16, 1.0, cfg) == [(-1, 24, 0, 40), (7, 24, 0, 8), (15, 24, 0, 8)]
     assert O.schedule(64, 0, 0.5, cfg) == [(-1, 20, 8, 36)]
     assert O.schedule(64, 0, 0.25, cfg) == [(-1, 14, 20, 30)]
 

@@ -510,8 +510,10 @@ def test_rho_zero_all_kept_tokens_quantized(layout):
 
 
 def test_minimal_budget_frequent_tailors():
-    """B = 2W + 1, the smallest budget R14 allows: a tailor every W + 1 steps keeping one
-    eligible token, no room left for Quantized tokens (schedule (32, 65, 98, ...))."""
+    """B = 2W + 1, the smallest budget R14 allows: a tailor every W steps (U reaches B_bytes
+    after exactly W appends, R12) keeping one eligible token, no room left for Quantized
+    tokens; the first decode tailor's window holds the W - 1 decode queries since the prompt
+    (R19)."""
     sh = Shape(batch=1, n_layers=1, n_q_heads=8, n_kv_heads=2, head_dim=128, prompt_len=300, window=32)
     r = run_parity(sh, budget=65, steps=100, seed=14, rho=[[0.5]], layout=2, bits=4, g=128, check_every=10)
     assert min(len(u.tailors) for u in r["ora"].units.values()) >= 4
