@@ -62,7 +62,7 @@ typedef struct arkv_config {
   int32_t n_layers;      /* L */
   int32_t n_q_heads;     /* H_q */
   int32_t n_kv_heads;    /* H_kv held by this process (G = H_q / H_kv, contiguous groups, R27) */
-  int32_t head_dim;      /* d, multiple of 16 */
+  int32_t head_dim;      /* d in {16, 32, 64, 128} (else ARKV_ERR_CONFIG) */
   int32_t batch;         /* sequences held by this process */
   int32_t window;        /* W, protected recency window (32 in P:368) */
   int32_t budget_tokens; /* B per (seq, layer, KV head) in bf16-token equivalents;
@@ -178,7 +178,14 @@ typedef struct arkv_unit_export {
 arkv_status arkv_export_unit(arkv_cache* cache, int32_t b, int32_t layer, int32_t kvh,
                              arkv_unit_export* out, void* stream);
 
-/* Syncs the stream and converts the device error flag into a status (and clears it). */
+/* Syncs the stream and converts the device error flag into a status (and clears it):
+   ARKV_ERR_DEVICE when, since the last check,
+     - a decode step's q, k or v held a non-finite bf16 value (Inf / NaN);
+     - a prompt K/V row entering the cache (kept by the prefill-end tailor, or ingested)
+       held one, or a NaN / Inf in q_win or K reached the Eq. 3 column sums or q_l;
+     - a slot would overflow (capacity) or a tailor's counts or positions disagreed with
+       the host schedule (integrity).
+   Evicted prompt V rows are never read and are not checked. */
 arkv_status arkv_check(arkv_cache* cache, void* stream);
 
 /* Host only.  Count schedule of one unit (R9, R12, R14, R15): prefill of prompt_len
@@ -233,7 +240,12 @@ arkv_status arkv_oq_score(const arkv_config* cfg, double entropy, double m2, dou
    stream around every launch (bench roofline).  arkv_profile(1) enables and resets;
    arkv_profile_read (syncs) returns the summed kernel time in ms, the number of timed
    launches and their summed algorithmic bytes (cache segments read + the step's token
-   read and appended + query read).  which = 0: decode attention kernel. */
+   read and appended + query read).  which = 0: decode attention kernel.
+   which = 1 (host only, no sync, always on): the algorithmic bytes of every arkv_decode_step
+   call since the cache was created (attention bytes as for which = 0 plus the
+   output written; + 16 B per row of units in their HH window; per tailor, 8 B per eligible
+   row + the unit's segments read once + the survivors written); launches = calls,
+   total_ms = 0. */
 arkv_status arkv_profile(arkv_cache* cache, int32_t enable);
 arkv_status arkv_profile_read(arkv_cache* cache, int32_t which, double* total_ms, int64_t* launches,
                               double* alg_bytes);

@@ -14,7 +14,9 @@ from typing import Dict, Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libarkv.so")
+# ARKV_LIBRARY: path of an A/B measurement build (libarkv_tuning.so, build.py --tuning);
+# bench.py records it and refuses to print a bench line with it set
+LIB_PATH = os.environ.get("ARKV_LIBRARY") or os.path.join(HERE, "libarkv.so")
 
 LAYOUT_AUTO, LAYOUT_PLAIN, LAYOUT_FRAG = 0, 1, 2
 QUANT_ASYM, QUANT_SYM, QUANT_FP8 = 0, 1, 2

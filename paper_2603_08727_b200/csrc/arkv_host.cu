@@ -16,6 +16,16 @@
 
 using namespace arkv;
 
+int arkv::tuning_knob(const char* name, int def) {
+#ifdef ARKV_TUNING_KNOBS
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : def;
+#else
+  (void)name;
+  return def;
+#endif
+}
+
 struct arkv_cache {
   arkv_config cfg;
   Geom g;
@@ -58,6 +68,10 @@ struct arkv_cache {
   std::vector<cudaEvent_t> ev;  // pairs
   std::vector<double> ev_bytes;
   int ev_used = 0;
+  // algorithmic bytes of every decode call since creation (host arithmetic, always on):
+  // arkv_profile_read(which = 1)
+  double step_bytes = 0.0;
+  int64_t step_calls = 0;
   bool fast = false;
   // host mirrors
   std::vector<double> rho;
@@ -97,7 +111,8 @@ arkv_status validate(const arkv_config* c) {
   if (c->n_q_heads % c->n_kv_heads) return ARKV_ERR_CONFIG;
   int G = c->n_q_heads / c->n_kv_heads;
   if (G != 1 && G != 2 && G != 4 && G != 8) return ARKV_ERR_CONFIG;
-  if (c->head_dim < 16 || c->head_dim > 256 || c->head_dim % 16) return ARKV_ERR_CONFIG;
+  // every kernel path (prefill passes, generic and fast decode, both move kernels) covers these
+  if (c->head_dim != 16 && c->head_dim != 32 && c->head_dim != 64 && c->head_dim != 128) return ARKV_ERR_CONFIG;
   if (c->quant_bits != 2 && c->quant_bits != 4 && c->quant_bits != 8) return ARKV_ERR_CONFIG;
   int gs = c->group_size ? c->group_size : c->head_dim;
   if (gs < 8 || gs % 8 || c->head_dim % gs) return ARKV_ERR_CONFIG;
@@ -227,9 +242,9 @@ int64_t appends_to_trigger(const Geom& g, int64_t n_o, int64_t n_q) {
 // queries before it, but only those that ran on the current cache (from q0 on).
 int acc0_of(const Geom& g, int64_t trig, int64_t q0) { return (int)std::max<int64_t>(trig - g.W, q0); }
 
-// ARKV_DEBUG_SYNC=1: synchronize after every launch group and name the failing one.
+// ARKV_DEBUG_SYNC=1 (tuning builds): synchronize after every launch group and name the failing one.
 void debug_sync(cudaStream_t s, const char* what) {
-  static const bool on = std::getenv("ARKV_DEBUG_SYNC") != nullptr;
+  static const bool on = tuning_knob("ARKV_DEBUG_SYNC", 0) != 0;
   if (!on) return;
   cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) std::fprintf(stderr, "arkv: %s failed: %s\n", what, cudaGetErrorString(e));
@@ -245,8 +260,8 @@ bool check_cuda(cudaError_t e) {
 extern "C" {
 
 const char* arkv_version(void) {
-  return "arkv 0.3 sm_100a layouts=plain,frag decode=generic,mma-sync-split,mma-sync-persistent "
-         "prefill=tcgen05-tma-ws,tcgen05,mma-sync quant=int2/4/8,fp8-e4m3 states=per-head,layer-shared "
+  return "arkv 0.4 sm_100a layouts=plain,frag decode=generic,mma-sync-split,mma-sync-persistent "
+         "prefill=tcgen05-tma-ws,mma-sync quant=int2/4/8,fp8-e4m3 states=per-head,layer-shared "
          "scores=eq9,smoothed";
 }
 
@@ -472,9 +487,9 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
     // small units (>= 32 per SM: split-K would run them as ~1-split CTAs in dozens of waves;
     // measured at configs[3], 16384 units: 35.7K vs 33.8K tok/s), else split-K (configs[1],
     // configs[2] per GPU, configs[4] per GPU: split-K 3-12 % faster).  ARKV_DECODE_PERSIST
-    // overrides the rule (measurement).
-    const char* e = std::getenv("ARKV_DECODE_PERSIST");
-    const bool auto_persist = e ? std::atoi(e) != 0 : s.g.n_units >= 32 * c->num_sms;
+    // overrides the rule (tuning builds).
+    const int ep = tuning_knob("ARKV_DECODE_PERSIST", -1);
+    const bool auto_persist = ep >= 0 ? ep != 0 : s.g.n_units >= 32 * c->num_sms;
     c->persist = c->fast && (cfg->decode_kernel == 3 || (cfg->decode_kernel == 0 && auto_persist));
   }
   if ((cfg->decode_kernel == 2 || cfg->decode_kernel == 3) && !fast_ok) {
@@ -518,7 +533,13 @@ arkv_status arkv_profile(arkv_cache* c, int32_t enable) {
 }
 
 arkv_status arkv_profile_read(arkv_cache* c, int32_t which, double* total_ms, int64_t* launches, double* alg_bytes) {
-  if (!c || which != 0) return ARKV_ERR_INVALID_ARG;
+  if (!c || which < 0 || which > 1) return ARKV_ERR_INVALID_ARG;
+  if (which == 1) {  // whole decode calls: host-side counts, no events, no sync
+    if (total_ms) *total_ms = 0.0;
+    if (launches) *launches = c->step_calls;
+    if (alg_bytes) *alg_bytes = c->step_bytes;
+    return ARKV_OK;
+  }
   double ms = 0.0, by = 0.0;
   for (int i = 0; i < c->ev_used; ++i) {
     if (!check_cuda(cudaEventSynchronize(c->ev[2 * i + 1]))) return ARKV_ERR_CUDA;
@@ -624,7 +645,7 @@ arkv_status arkv_prefill_finish(arkv_cache* c, const void* k, const void* v, int
   std::vector<double> rho(BL, 1.0);
   if (stats_ok) {
     double* oq = d_oq ? d_oq : c->oq_tmp;
-    int nl = launch_prefill_finish(g, d_colsum ? d_colsum : c->colsum, P, d_stats, oq, c->cfg.tau, c->cfg.stat_eps, s);
+    int nl = launch_prefill_finish(g, d_colsum ? d_colsum : c->colsum, P, d_stats, oq, c->cfg.tau, c->cfg.stat_eps, c->err, s);
     c->launches += nl;
     debug_sync(s, "prefill_finish");
     if (!check_cuda(cudaGetLastError())) return ARKV_ERR_CUDA;
@@ -896,7 +917,7 @@ arkv_status arkv_persist_plan_check(const arkv_config* cfg, const int32_t* n_o, 
   PersistPlan* plan = new PersistPlan();
   build_plan_counts(s.g, n_units, n_o, n_q, max_ctas, plan);
   const bool ok = replay_plan(s.g, n_units, n_o, n_q, *plan);
-  if (!ok && std::getenv("ARKV_DEBUG_PLAN")) std::fprintf(stderr, "replay_plan: violation at arkv_host.cu:%d\n", fail_line);
+  if (!ok && tuning_knob("ARKV_DEBUG_PLAN", 0)) std::fprintf(stderr, "replay_plan: violation at arkv_host.cu:%d\n", fail_line);
   if (ctas_used) *ctas_used = plan->P;
   delete plan;
   return ok ? ARKV_OK : ARKV_ERR_DEVICE;
@@ -1001,6 +1022,11 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
         int64_t oe, qn;
         tailor_counts(g, c->cfg.alpha, K, c->rho[bl], &oe, &qn);
         const int n_o_after = (int)oe + g.W;  // after this step's append
+        // tailor: the eligible rows' accumulators, the unit's segments read
+        // once, the survivors written
+        c->step_bytes += (double)g.Hkv * (8.0 * (double)(K - g.W) + (double)c->n_o[bl] * g.cost_o +
+                                          (double)c->n_q[bl] * g.cost_q + (double)n_o_after * g.cost_o +
+                                          (double)qn * g.cost_q);
         const int trig_new = (int)(t + appends_to_trigger(g, n_o_after, qn));
         for (int kvh = 0; kvh < g.Hkv; ++kvh) {
           TailorJob jb{};
@@ -1030,9 +1056,13 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
       }
       const int tiles = (c->n_o[bl] + 1 + kTile - 1) / kTile + (c->n_q[bl] + kTile - 1) / kTile;
       max_tiles = std::max(max_tiles, tiles);
+      // attention: segments read, the token read and appended, q read, out written
+      c->step_bytes += (double)g.Hkv * ((double)c->n_o[bl] * g.cost_o + (double)c->n_q[bl] * g.cost_q +
+                                        2.0 * g.cost_o + 4.0 * g.G * g.d);
       const int acc0 = acc0_of(g, c->trig[bl], c->q0[bl]);
       if (t >= acc0 && t < c->trig[bl]) {  // HH accumulation step (R19)
         const int rows = c->n_o[bl] + 1 + c->n_q[bl];
+        c->step_bytes += (double)g.Hkv * 16.0 * rows;  // accumulator read-modify-write
         acc_rows = std::max(acc_rows, rows);
         if (hh.n < kMaxHhEntries)
           hh.e[hh.n++] = make_int4(b * n_layers + (l - layer0), rows, t == acc0 ? 1 : 0, c->n_q[bl]);
@@ -1040,12 +1070,8 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
           hh_fit = false;
       }
     }
-  // ARKV_TIMING_SKIP (timing experiments only; results are wrong): bit 0 skips the tailor
-  // launches, bit 1 the HH accumulation, bit 2 the split combine, so a bench run isolates
-  // their share of a step
-  static const int skip = std::getenv("ARKV_TIMING_SKIP") ? std::atoi(std::getenv("ARKV_TIMING_SKIP")) : 0;
-  if (skip & 2) acc_rows = 0;
-  if (!jobs.empty() && !(skip & 1)) {
+  ++c->step_calls;
+  if (!jobs.empty()) {
     arkv_status st = run_jobs(c, jobs, nullptr, nullptr, 0, s);
     c->ext_scores = nullptr;  // consumed (also when this step runs no tailor: see below)
     if (st != ARKV_OK) return st;
@@ -1057,10 +1083,7 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   const int slots = c->num_sms * (c->fast ? 2 : 4);
   int S = (int)std::lround(2.6 * slots / (double)n_units_call);
   S = std::max(1, std::min(S, std::min(c->max_splits, max_tiles)));
-  if (const char* env = std::getenv("ARKV_SPLITS")) {  // tuning knob (bench sweeps)
-    const int v = std::atoi(env);
-    if (v > 0) S = std::min(v, std::min(c->max_splits, max_tiles));
-  }
+  if (const int v = tuning_knob("ARKV_SPLITS", 0); v > 0) S = std::min(v, std::min(c->max_splits, max_tiles));
 
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->prof && 2 * (c->ev_used + 1) <= (int)c->ev.size()) {
@@ -1079,7 +1102,7 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
     c->ev_used++;
   }
   PlanArgs pa;
-  static const bool fuse_hh = !std::getenv("ARKV_FUSE_HH") || std::atoi(std::getenv("ARKV_FUSE_HH")) != 0;
+  static const bool fuse_hh = tuning_knob("ARKV_FUSE_HH", 1) != 0;
   if (acc_rows > 0 && hh_fit && fuse_hh && !c->persist) {
     hh.n_units = g.batch * n_layers * g.Hkv;
     pa.hh = &hh;

@@ -248,10 +248,66 @@ __host__ __device__ inline bool q_code_slot(const Geom& g, int B, int s, int* j,
 // Programmatic dependent launch: a kernel launched with programmatic stream
 // serialization may start while its predecessor drains; it must wait before touching
 // memory the predecessor writes.  Both are no-ops for ordinary launches.
+// L2 residency hints (createpolicy + .L2::cache_hint).  The HH window's logits and
+// accumulators (~70 MB at configs[1]) are kept resident with evict_last while the cache
+// tiles stream through with evict_first, so the logit round trip between the decode kernel
+// and the HH combine stays in the 126 MB L2 instead of HBM.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;\n" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(float2* p, float2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;\n" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ float ld_hint(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;\n" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ld_hint4(const float* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float2 ld_hint(const float2* p, uint64_t pol) {
+  float2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;\n" : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 __device__ __forceinline__ float bf16_to_f(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+// Non-finite bf16 inputs (Inf, NaN: all-ones exponent) — SPEC S:329 "non-finite input ->
+// numeric error", raised through kErrNonFinite and arkv_check (include/arkv.h).
+__device__ __forceinline__ bool bf16_nonfinite(uint16_t b) { return (b & 0x7F80u) == 0x7F80u; }
+__device__ __forceinline__ bool bf16x2_nonfinite(uint32_t w) {
+  const uint32_t t = ~w & 0x7F807F80u;  // a half is non-finite iff its exponent bits are all set
+  return (t & 0xFFFFu) == 0u || (t >> 16) == 0u;
+}
+__device__ __forceinline__ bool bf16x8_nonfinite(const uint4& v) {
+  return bf16x2_nonfinite(v.x) | bf16x2_nonfinite(v.y) | bf16x2_nonfinite(v.z) | bf16x2_nonfinite(v.w);
+}
+// One warp checks the step's q rows (n_q elements) and new k/v rows (n_kv elements each).
+__device__ __forceinline__ bool warp_step_nonfinite(const uint16_t* q, int n_q, const uint16_t* k, const uint16_t* v,
+                                                    int n_kv, int lane) {
+  bool bad = false;
+  for (int i = lane; i < n_q; i += 32) bad |= bf16_nonfinite(q[i]);
+  for (int i = lane; i < n_kv; i += 32) bad |= bf16_nonfinite(k[i]) | bf16_nonfinite(v[i]);
+  return __any_sync(0xffffffffu, bad);
+}
 
 // The number a stored Quantized code stands for (R23): the integer (minus the symmetric
 // offset), or the e4m3 value of an fp8 code (NEXT-2).

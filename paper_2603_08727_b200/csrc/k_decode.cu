@@ -84,6 +84,8 @@ __global__ void __launch_bounds__(128) decode_split_generic(DecodeArgs a) {
 
   // Append the step's token (D1) — by the CTA owning the last Original tile.
   if (o0 <= n_o / kTile && n_o / kTile < o1 && warp == 0) {
+    // non-finite q / k / v of the step
+    if (warp_step_nonfinite(qp, G * d, kn, vn, d, lane) && lane == 0) atomicOr(a.err, kErrNonFinite);
     const int tt = n_o / kTile, j = n_o % kTile;
     bool fits = (n_o + 1 <= g.cap_o) &&
                 ((int64_t)tiles_o * g.tile_o + (int64_t)tiles_q * g.tile_q <= g.slot_bytes);
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(128) decode_split_generic(DecodeArgs a) {
         if (accm && ld == 0) {
           const int ridx = isq ? g.cap_o + row : row;
 #pragma unroll
-          for (int h = 0; h < G; ++h) a.logits[((int64_t)u * G + h) * row_stride + ridx] = sc[h];
+          for (int h = 0; h < G; ++h) a.logits[((int64_t)u * row_stride + ridx) * G + h] = sc[h];
         }
 #pragma unroll
         for (int h = 0; h < G; ++h) {
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(256) decode_hh_acc(DecodeArgs a) {
   float a1 = 0.f, a2 = 0.f;
 #pragma unroll
   for (int h = 0; h < G; ++h) {
-    const float p = exp2f(a.logits[((int64_t)u * G + h) * row_stride + ridx] - M[h]) * IL[h];
+    const float p = exp2f(a.logits[((int64_t)u * row_stride + ridx) * G + h] - M[h]) * IL[h];
     a1 += p;
     a2 += p * p;
   }
@@ -323,16 +325,26 @@ __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const Hh
   // logits do not depend on them): kHhRowsPerThread rows x (G logits + acc) in flight
   float lg[kHhRowsPerThread][G];
   float2 ac[kHhRowsPerThread];
+  const uint64_t pol = l2_evict_last();  // logits and accumulators stay L2-resident over the window
 #pragma unroll
   for (int k = 0; k < kHhRowsPerThread; ++k) {
     const int i = r0 + threadIdx.x + k * blockDim.x;
     const bool ok = i < n_rows;
     const bool isq = i >= n_o;
     const int ridx = isq ? g.cap_o + (i - n_o) : i;
+    const float* lp = a.logits + ((int64_t)u * row_stride + ridx) * G;  // the row's G logits: one vector load
+    if constexpr (G == 4) {
+      const float4 v4 = ok ? ld_hint4(lp, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
+      lg[k][0] = v4.x;
+      lg[k][1] = v4.y;
+      lg[k][2] = v4.z;
+      lg[k][3] = v4.w;
+    } else {
 #pragma unroll
-    for (int h = 0; h < G; ++h) lg[k][h] = ok ? __ldcs(a.logits + ((int64_t)u * G + h) * row_stride + ridx) : 0.f;
+      for (int h = 0; h < G; ++h) lg[k][h] = ok ? ld_hint(lp + h, pol) : 0.f;
+    }
     ac[k] = make_float2(0.f, 0.f);
-    if (ok && !first) ac[k] = isq ? sm.acc_q[i - n_o] : sm.acc_o[i];
+    if (ok && !first) ac[k] = ld_hint(isq ? &sm.acc_q[i - n_o] : &sm.acc_o[i], pol);
   }
   __shared__ float sM[G], sIL[G];
   if ((int)threadIdx.x < G) {
@@ -355,7 +367,7 @@ __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const Hh
       a2 += p * p;
     }
     float2* ap = i >= n_o ? &sm.acc_q[i - n_o] : &sm.acc_o[i];
-    *ap = make_float2(ac[k].x + a1, ac[k].y + a2);
+    st_hint(ap, make_float2(ac[k].x + a1, ac[k].y + a2), pol);
   }
 }
 
@@ -449,16 +461,12 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
   a.mstat = mstat;
   a.counters = counters;
   {
-    const char* e1 = std::getenv("ARKV_QGROUP");
-    const char* e2 = std::getenv("ARKV_INTERLEAVE");
-    a.q_group = e1 ? std::atoi(e1) : 0;           // default: as many Q tiles as fit a stage
-    a.interleave = e2 ? std::atoi(e2) : 0;        // measured: interleaving O/Q items is slower
-    const char* e3 = std::getenv("ARKV_FUSE_COMBINE");
-    a.fuse_combine = e3 ? std::atoi(e3) : 0;      // measured: the separate combine kernel is faster
-    const char* e5 = std::getenv("ARKV_PREFETCH");
-    a.prefetch = e5 ? std::atoi(e5) : 0;
-    const char* e4 = std::getenv("ARKV_ITEM_ORDER");
-    a.item_order = e4 ? std::atoi(e4) : 1;  // measured: alternating O-first / Q-first CTAs -1.2 %
+    a.q_group = tuning_knob("ARKV_QGROUP", 0);          // default: as many Q tiles as fit a stage
+    a.interleave = tuning_knob("ARKV_INTERLEAVE", 0);   // measured: interleaving O/Q items is slower
+    a.fuse_combine = tuning_knob("ARKV_FUSE_COMBINE", 0);  // measured: the separate combine kernel is faster
+    a.prefetch = tuning_knob("ARKV_PREFETCH", 0);
+    a.item_order = tuning_knob("ARKV_ITEM_ORDER", 1);   // measured: alternating O-first / Q-first CTAs -1.2 %
+    a.l2_hints = tuning_knob("ARKV_L2_HINTS", 1);
   }
   a.out = out;
   a.out_fp32 = out_fp32;

@@ -80,6 +80,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// ... with an L2 eviction policy (cache tiles are read once per step: evict_first)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 // Bulk prefetch of [src, src + bytes) into L2 (no completion tracking).
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
@@ -162,10 +171,11 @@ __device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint32_t v16) {
 }
 __device__ __forceinline__ uint32_t e4m3x2_lo(uint32_t w) { return e4m3x2_to_f16x2(w); }
 __device__ __forceinline__ uint32_t e4m3x2_hi(uint32_t w) { return e4m3x2_to_f16x2(w >> 16); }
-// The same without the exact "- 1024": codes stay as f16 (1024 + c) / (1024 + 16c).  Used
-// for the PV contraction only, whose result tolerates the fp32 cancellation of the offset
-// (~1e-5 absolute on the output); the logits (QK), which decide token states through the
-// heavy-hitter scores, keep the exact unpack.
+// The same without the exact "- 1024": codes stay as f16 (1024 + c) / (1024 + 16c), the
+// offset removed later in the fp32 zero-point term.  OFF by default (ARKV_PV_RAW=0): the
+// PV accumulator then carries ~1024x the output's magnitude, and the fp32 cancellation
+// grew to 1.5e-3 absolute at 32K contexts with ~17K Quantized tokens (round 2, full-size
+// parity: at the tolerance); the exact unpack costs +0.8 % decode-kernel time.
 __device__ __forceinline__ void unpack8_raw(uint32_t w, uint32_t (&x)[4]) {
   const uint32_t w8 = w >> 8;
   x[0] = lop3_mask_or(w, 0x000F000Fu, 0x64006400u);
@@ -174,7 +184,7 @@ __device__ __forceinline__ void unpack8_raw(uint32_t w, uint32_t (&x)[4]) {
   x[3] = lop3_mask_or(w8, 0x00F000F0u, 0x64006400u);
 }
 #ifndef ARKV_PV_RAW
-#define ARKV_PV_RAW 1
+#define ARKV_PV_RAW 0
 #endif
 constexpr bool kPvRaw = ARKV_PV_RAW != 0;
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -342,10 +352,11 @@ __device__ __forceinline__ void acc_reset(Acc<NG>& s) {
 }
 
 // Folds one staged 32-token tile into the warp's flash state.  tb: the tile in shared
-// memory; n_valid: rows in use; lrow: HH logit row base of this tile (a.logits + (u G)
-// row_stride + (isq ? cap_o : 0) + 32 tile) or nullptr outside the HH window.
+// memory; n_valid: rows in use; lrow: HH logits of this tile's first row, [row][G] (a.logits
+// + (u row_stride + (isq ? cap_o : 0) + 32 tile) G) or nullptr outside the HH window.
 template <int G, int NG, bool F8>
 __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_valid, float* lrow, int row_stride,
+                                             uint64_t lpol,
                                              const QFrag<NG>& f, Acc<NG>& s, float c2, bool sym, int lane,
                                              int src_lane) {
   const int gq = lane >> 2, tq = lane & 3;
@@ -470,13 +481,20 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
       if (j >= n_valid || h >= G) lg[mt][e] = -INFINITY;
     }
   if (lrow) {
+    // logits [row][G]: this lane's heads 2t, 2t+1 of a row are adjacent — one 8-byte store
+    // per (m-tile, row half); the 8 rows x G heads of one store instruction are contiguous
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = mt * 16 + gq + 8 * (e >> 1);
-        const int h = 2 * tq + (e & 1);
-        if (j < n_valid && h < G) lrow[(int64_t)h * row_stride + j] = lg[mt][e];
+      for (int hh = 0; hh < 2; ++hh) {
+        const int j = mt * 16 + gq + 8 * hh;
+        if (j < n_valid && 2 * tq < G) {
+          float* p = lrow + j * G + 2 * tq;
+          if (G >= 2)
+            st_hint((float2*)p, make_float2(lg[mt][2 * hh], lg[mt][2 * hh + 1]), lpol);
+          else
+            st_hint(p, lg[mt][2 * hh], lpol);
+        }
       }
   }
   // ---- online softmax (per head = per (tq, e)) ----
@@ -721,6 +739,7 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
   if (warp == kConsumers) {
     // ===================== producer =====================
     if (lane == 0) {
+      const uint64_t pol_stream = l2_evict_first();
       // items in order (measured: polling stages out of order and busy-waiting costs the
       // co-scheduled consumer warp issue slots; try_wait suspends in hardware)
       auto item_src = [&](int i, const uint8_t*& src, uint32_t& bytes) {
@@ -750,13 +769,18 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
         uint32_t bytes;
         item_src(i, src, bytes);
         mbar_expect_tx(&sm.full[st], bytes);
-        bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
+        if (a.l2_hints)
+          bulk_g2s_hint(sm.ring[st], src, bytes, &sm.full[st], pol_stream);
+        else
+          bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
       }
       griddep_launch_dependents();  // PDL: the combine may start launching (it waits for us)
     }
     __syncwarp();  // reconverge before warp-collective code and the aligned CTA barrier
     // the producer warp also appends the step's token (D1) when this CTA owns its tile
     if (owns_new) {
+      // non-finite q / k / v of the step
+      if (warp_step_nonfinite(qp, G * D, kn, vn, D, lane) && lane == 0) atomicOr(a.err, kErrNonFinite);
       const int tt = n_o / kTile, j = n_o % kTile;
       const SlotMeta meta = slot_meta(a.meta, g, dsc.slot);
       const bool fits = (n_o + 1 <= g.cap_o) &&
@@ -789,10 +813,11 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
       }
       __syncwarp();
       if (accm && lane < G)
-        a.logits[((int64_t)u * G + lane) * row_stride + n_o] = sm.newtok[0][lane];
+        st_hint(a.logits + ((int64_t)u * row_stride + n_o) * G + lane, sm.newtok[0][lane], l2_evict_last());
     }
   } else {
     // ===================== consumers =====================
+    const uint64_t lpol = l2_evict_last();  // HH logits stay in L2 for the combine
     QFrag<NG> qf;
     load_qfrag<G, NG, F8>(qp, lane, qf);
     Acc<NG> acc;
@@ -812,8 +837,9 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
         const uint8_t* tb = sm.ring[st] + (isq ? (ntiles - 1 - jt) * g.tile_q : 0);
         const int tile = first + jt;
         const int n_valid = isq ? min(kTile, n_q - tile * kTile) : min(kTile, n_o - tile * kTile);
-        float* lrow = accm ? a.logits + (int64_t)u * G * row_stride + (isq ? g.cap_o : 0) + tile * kTile : nullptr;
-        consume_tile<G, NG, F8>(tb, isq, n_valid, lrow, row_stride, qf, acc, c2, sym, lane, src_lane);
+        float* lrow =
+            accm ? a.logits + ((int64_t)u * row_stride + (isq ? g.cap_o : 0) + tile * kTile) * G : nullptr;
+        consume_tile<G, NG, F8>(tb, isq, n_valid, lrow, row_stride, lpol, qf, acc, c2, sym, lane, src_lane);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[st]);
@@ -900,10 +926,10 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
 
 template <int G, int NG, int C, int SPW, bool F8 = false>
 static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
-  auto kern = decode_fast_kernel<G, NG, C, SPW, F8>;
   const int smem = (int)sizeof(Smem<C, SPW>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   dim3 grid(a.n_splits, n_units_call);
+  auto kern = decode_fast_kernel<G, NG, C, SPW, F8>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (ev0) cudaEventRecord(ev0, s);
   launch_pdl(kern, grid, dim3((C + 1) * 32), (size_t)smem, s, a);
   if (ev1) cudaEventRecord(ev1, s);
@@ -914,21 +940,17 @@ static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
 // stage per warp, the warp waited a full HBM round trip per item: 21 % of the stall
 // samples of the Base_quant profile).  Measured at configs[1]: kernel 0.1693 -> 0.1565 ms
 // vs 4 x 1.  For the paper's shape (G = 4, one group) alternatives are selectable for
-// measurement with ARKV_FAST_CFG=C,SPW (4,1 | 4,2 | 6,2 | 4,3 | 8,1 | 2,2 | 2,3).
+// measurement in tuning builds (-DARKV_TUNING_KNOBS) with ARKV_FAST_CFG=10*C+SPW (41 | 42 | 62 |
+// 43 | 81 | 22 | 23); the shipped library instantiates only the default.
 template <int G, int NG>
 static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
   if (a.g.mode == ARKV_QUANT_FP8) {
-    const char* e = std::getenv("ARKV_FAST_CFG");
-    if (e && e[0] == '4')
-      launch_cfg<G, NG, 4, 1, true>(a, n_units_call, s, ev0, ev1);
-    else
-      launch_cfg<G, NG, 3, 2, true>(a, n_units_call, s, ev0, ev1);
+    launch_cfg<G, NG, 3, 2, true>(a, n_units_call, s, ev0, ev1);
     return;
   }
+#ifdef ARKV_TUNING_KNOBS
   if (G == 4 && NG == 1) {
-    const char* e = std::getenv("ARKV_FAST_CFG");
-    const int cfg = e ? (e[0] - '0') * 10 + (e[2] - '0') : 32;
-    switch (cfg) {
+    switch (tuning_knob("ARKV_FAST_CFG", 32)) {
       case 42: launch_cfg<G, NG, 4, 2>(a, n_units_call, s, ev0, ev1); return;
       case 62: launch_cfg<G, NG, 6, 2>(a, n_units_call, s, ev0, ev1); return;
       case 43: launch_cfg<G, NG, 4, 3>(a, n_units_call, s, ev0, ev1); return;
@@ -939,6 +961,7 @@ static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cud
       default: break;
     }
   }
+#endif
   launch_cfg<G, NG, 3, 2>(a, n_units_call, s, ev0, ev1);
 }
 
@@ -1074,6 +1097,7 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
     // ============ producer: merges the two ranges by unit (a unit's Original tiles, then
     // its Quantized groups) so each consumer warp accumulates a unit across both kinds ============
     if (lane == 0) {
+      const uint64_t pol_stream = l2_evict_first();
       Walker w0, w1;
       w0.init(a, plan.cta[0][c], 0, q_per, n_units_call);
       w1.init(a, plan.cta[1][c], 1, q_per, n_units_call);
@@ -1099,7 +1123,10 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
           bytes = (uint32_t)(nt * g.tile_q);
         }
         mbar_expect_tx(&sm.full[st], bytes);  // release: orders the info writes above
-        bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
+        if (a.l2_hints)
+          bulk_g2s_hint(sm.ring[st], src, bytes, &sm.full[st], pol_stream);
+        else
+          bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
       };
       // per unit: Original tiles first on even CTAs, Quantized groups first on odd ones, so
       // co-resident CTAs tend to overlap HBM-bound and ALU-heavy work
@@ -1164,6 +1191,7 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
       }
     }
   };
+  const uint64_t lpol = l2_evict_last();  // HH logits stay in L2 for the combine
   for (int j = warp; j < n_work; j += C) {
     constexpr int NS = PSmem<C>::kSt;
     const int st = j % NS;
@@ -1177,17 +1205,17 @@ __global__ void __launch_bounds__((kPersistConsumers + 1) * 32, 2)
       acc_reset(acc);
     }
     const int u = i0.y, k = i0.z;
-    float* lbase = i1.w ? a.logits + (int64_t)u * G * row_stride : nullptr;
+    float* lbase = i1.w ? a.logits + (int64_t)u * row_stride * G : nullptr;
     if (i0.w == 0) {
-      consume_tile<G, NG, F8>(sm.ring[st], false, min(kTile, i1.x - k * kTile), lbase ? lbase + k * kTile : nullptr,
-                          row_stride, qf, acc, c2, sym, lane, src_lane);
+      consume_tile<G, NG, F8>(sm.ring[st], false, min(kTile, i1.x - k * kTile), lbase ? lbase + k * kTile * G : nullptr,
+                          row_stride, lpol, qf, acc, c2, sym, lane, src_lane);
     } else {
       const int first = k * q_per, nt = min(q_per, i1.z - first);
       for (int jt = 0; jt < nt; ++jt) {
         const int tile = first + jt;
         consume_tile<G, NG, F8>(sm.ring[st] + (nt - 1 - jt) * g.tile_q, true, min(kTile, i1.y - tile * kTile),
-                            lbase ? lbase + g.cap_o + tile * kTile : nullptr, row_stride, qf, acc, c2, sym, lane,
-                            src_lane);
+                            lbase ? lbase + (g.cap_o + tile * kTile) * G : nullptr, row_stride, lpol, qf, acc,
+                            c2, sym, lane, src_lane);
       }
     }
     __syncwarp();
@@ -1227,6 +1255,8 @@ __global__ void __launch_bounds__(G * D) decode_persist_combine(DecodeArgs a) {
   if (tid < 4) s_cov[tid] = a.pcover[(tid >> 1) * 2 * n_units_call + (tid & 1) * n_units_call + ul];
   // ---- append the token to the Original stack (row n_o) ----
   const uint16_t vx = vn[x];
+  // non-finite q / k / v of the step
+  if (bf16_nonfinite(qp[tid]) || (h == 0 && (bf16_nonfinite(kn[x]) || bf16_nonfinite(vx)))) atomicOr(a.err, kErrNonFinite);
   if (h == 0) {
     const int tiles_o = (n_o + 1 + kTile - 1) / kTile, tiles_q = (dsc.n_q + kTile - 1) / kTile;
     const bool fits =
@@ -1255,7 +1285,7 @@ __global__ void __launch_bounds__(G * D) decode_persist_combine(DecodeArgs a) {
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
       s_new[h] = acc * c2;
-      if (accm) a.logits[((int64_t)u * G + h) * row_stride + n_o] = acc * c2;
+      if (accm) st_hint(a.logits + ((int64_t)u * row_stride + n_o) * G + h, acc * c2, l2_evict_last());
     }
   }
   __syncthreads();
@@ -1397,9 +1427,6 @@ int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
   }
   if (r < 0) return -1;
   if (a.fuse_combine) return 1;  // the last split CTA of each unit merged the partials
-  // ARKV_TIMING_SKIP bit 2 (timing experiments only, results wrong): no combine
-  static const int skip = std::getenv("ARKV_TIMING_SKIP") ? std::atoi(std::getenv("ARKV_TIMING_SKIP")) : 0;
-  if (skip & 4) return 1;
   if (hh) {
     launch_decode_combine_hh(a, *hh, acc_rows, s);
     return 102;

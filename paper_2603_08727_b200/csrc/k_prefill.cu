@@ -304,7 +304,8 @@ __global__ void prefill_colsum_kernel(Geom g, const float2* __restrict__ acc_pf,
 
 __global__ void __launch_bounds__(1024) prefill_moments_kernel(Geom g, const double* __restrict__ colsum, int P,
                                                                double* __restrict__ stats, double* __restrict__ oq,
-                                                               double t1, double t2, double t3, double eps) {
+                                                               double t1, double t2, double t3, double eps,
+                                                               int32_t* err) {
   __shared__ double sh[33];
   const int bl = blockIdx.x;
   const int n = P - g.W;
@@ -333,7 +334,10 @@ __global__ void __launch_bounds__(1024) prefill_moments_kernel(Geom g, const dou
       stats[bl * 3 + 1] = Vc;
       stats[bl * 3 + 2] = Kc;
     }
-    oq[bl] = pow(Hc, 1.0 / t1) * pow(Vc, 1.0 / t2) * pow(Kc, 1.0 / t3);  // Eq. 6
+    const double q = pow(Hc, 1.0 / t1) * pow(Vc, 1.0 / t2) * pow(Kc, 1.0 / t3);  // Eq. 6
+    oq[bl] = q;
+    // a NaN / Inf in q_win or K reaches the column sums
+    if (!isfinite(Z) || !isfinite(q)) atomicOr(err, kErrNonFinite);
   }
 }
 
@@ -359,29 +363,24 @@ static int launch_passes(const Geom& g, const uint16_t* q_win, const uint16_t* k
   return 2;
 }
 
-bool prefill_tc_available(const Geom& g);  // k_prefill_tc.cu
+bool prefill_ws_available(const Geom& g);  // k_prefill_ws.cu
 int launch_prefill_ws(const Geom& g, const uint16_t* q_win, const uint16_t* k, int P, float2* partials, int n_chunks1,
                       float2* acc_pf, int num_sms, cudaStream_t s);  // k_prefill_ws.cu
-int launch_prefill_tc(const Geom& g, const uint16_t* q_win, const uint16_t* k, int P, float2* partials, int n_chunks1,
-                      float2* acc_pf, cudaStream_t s);
 
 int launch_prefill_begin(const Geom& g, const uint16_t* q_win, const uint16_t* k, int P, float* partials,
                          int n_chunks1, float2* acc_pf, double* colsum, cudaStream_t s) {
-  // ARKV_PREFILL_TC: '0' mma.sync passes, '1' the first tcgen05 kernel (one CTA per chunk),
-  // default the warp-specialised persistent tcgen05 kernel (k_prefill_ws.cu)
-  const char* env = std::getenv("ARKV_PREFILL_TC");
-  if (prefill_tc_available(g) && !(env && env[0] == '0')) {  // tcgen05 passes (G*W = 128, d = 128)
-    int n = -1;
-    if (!(env && env[0] == '1')) {
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      n = launch_prefill_ws(g, q_win, k, P, (float2*)partials, n_chunks1, acc_pf, sms, s);
+  // the warp-specialised persistent tcgen05 kernel (k_prefill_ws.cu) for G*W = 128, d = 128;
+  // the mma.sync passes below for every other shape (ARKV_PREFILL_MMA=1 in tuning builds)
+  if (prefill_ws_available(g) && tuning_knob("ARKV_PREFILL_MMA", 0) == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int n = launch_prefill_ws(g, q_win, k, P, (float2*)partials, n_chunks1, acc_pf, sms, s);
+    if (n >= 0) {
+      dim3 grid((P - g.W + 255) / 256, g.batch * g.L);
+      prefill_colsum_kernel<<<grid, 256, 0, s>>>(g, acc_pf, P, colsum);
+      return n + 1;
     }
-    if (n < 0) n = launch_prefill_tc(g, q_win, k, P, (float2*)partials, n_chunks1, acc_pf, s);
-    dim3 grid((P - g.W + 255) / 256, g.batch * g.L);
-    prefill_colsum_kernel<<<grid, 256, 0, s>>>(g, acc_pf, P, colsum);
-    return n + 1;
   }
   const int R = g.G * g.W;
   const int mtiles = (R + 15) / 16;
@@ -408,8 +407,9 @@ int launch_prefill_begin(const Geom& g, const uint16_t* q_win, const uint16_t* k
 }
 
 int launch_prefill_finish(const Geom& g, const double* colsum, int P, double* stats, double* oq, const double* tau,
-                          double stat_eps, cudaStream_t s) {
-  prefill_moments_kernel<<<g.batch * g.L, 1024, 0, s>>>(g, colsum, P, stats, oq, tau[0], tau[1], tau[2], stat_eps);
+                          double stat_eps, int32_t* err, cudaStream_t s) {
+  prefill_moments_kernel<<<g.batch * g.L, 1024, 0, s>>>(g, colsum, P, stats, oq, tau[0], tau[1], tau[2], stat_eps,
+                                                         err);
   return 1;
 }
 

@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
                                                           const uint16_t* __restrict__ pk,
                                                           const uint16_t* __restrict__ pv, int P,
                                                           const int32_t* __restrict__ src_scratch, int src_stride,
-                                                          const float* __restrict__ ssm) {
+                                                          const float* __restrict__ ssm, int32_t* err) {
   extern __shared__ __align__(16) uint8_t tile[];
   griddep_wait();
   Geom g = g_in;
@@ -497,6 +497,7 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
         if (kind == kSrcInput) {
           kx = bf16_to_f(upk[(int64_t)orow * g.d + x]);
           vx = bf16_to_f(upv[(int64_t)orow * g.d + x]);
+          if (!isfinite(kx) || !isfinite(vx)) atomicOr(err, kErrNonFinite);
         } else if (kind == kSrcOldO) {
           kx = read_o(g, ot, oj, x, false);
           vx = read_o(g, ot, oj, x, true);
@@ -621,7 +622,8 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
                                                                uint8_t* meta, const uint16_t* __restrict__ pk,
                                                                const uint16_t* __restrict__ pv, int P,
                                                                const int32_t* __restrict__ src_scratch,
-                                                               int src_stride, const float* __restrict__ ssm) {
+                                                               int src_stride, const float* __restrict__ ssm,
+                                                               int32_t* err) {
   using namespace mvf;
   __shared__ __align__(16) Smem sm;
   griddep_wait();
@@ -677,6 +679,7 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
     }
   }
   // ---- phase 1: one warp per row ----
+  bool nonfinite = false;
   for (int j = warp, r = 0; j < kTile; j += 8, ++r) {
     const int row = tid * kTile + j;
     const int32_t sref = __shfl_sync(0xffffffffu, my_sref, r);
@@ -711,7 +714,9 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
     } else if (kind == kSrcInput) {
       // prompt row: 16 lanes x 16 B of K, 16 lanes x 16 B of V
       const uint16_t* rowp = (lane < 16 ? upk : upv) + (int64_t)orow * D + (lane & 15) * 8;
-      *(uint4*)&sm.stage[lane >> 4][j][(lane & 15) * 8] = *(const uint4*)rowp;
+      const uint4 pr = *(const uint4*)rowp;
+      *(uint4*)&sm.stage[lane >> 4][j][(lane & 15) * 8] = pr;
+      nonfinite |= bf16x8_nonfinite(pr);  // prompt values entering the cache
     } else {
       // old Original row: K quad (t, q) holds dims 32t + 8q .. +7 of the token (FRAG K map)
       const uint8_t* ot = o_tile_ptr((uint8_t*)oslot, g, orow >> 5);
@@ -783,6 +788,7 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
     }
     if (lane % LPG == 0) sm.sc[j][lane / LPG] = scv;
   }
+  if (nonfinite) atomicOr(err, kErrNonFinite);
   __syncthreads();
 
   // ---- phase 2: 16-byte output quads straight to HBM ----
@@ -875,16 +881,16 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
              src_scratch, src_stride, err);
   dim3 grid(max_tiles, n_jobs);
   const float* ssm = g.smooth > 0.f ? shs.ssm : nullptr;
-  if (g.layout == ARKV_LAYOUT_FRAG && g.d == mvf::D && g.bits == 4 && std::getenv("ARKV_MOVE_GENERIC") == nullptr) {
+  if (g.layout == ARKV_LAYOUT_FRAG && g.d == mvf::D && g.bits == 4 && tuning_knob("ARKV_MOVE_GENERIC", 0) == 0) {
     switch (g.ng) {
       case 1: launch_pdl(tailor_move_frag_kernel<1>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride, ssm); return 3 + extra;
+                         (const int32_t*)src_scratch, src_stride, ssm, err); return 3 + extra;
       case 2: launch_pdl(tailor_move_frag_kernel<2>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride, ssm); return 3 + extra;
+                         (const int32_t*)src_scratch, src_stride, ssm, err); return 3 + extra;
       case 4: launch_pdl(tailor_move_frag_kernel<4>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride, ssm); return 3 + extra;
+                         (const int32_t*)src_scratch, src_stride, ssm, err); return 3 + extra;
       case 8: launch_pdl(tailor_move_frag_kernel<8>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride, ssm); return 3 + extra;
+                         (const int32_t*)src_scratch, src_stride, ssm, err); return 3 + extra;
       default: break;
     }
   }
@@ -893,7 +899,7 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
 #define MV_LAUNCH(V, DCV)                                                                                         \
   cudaFuncSetAttribute(tailor_move_kernel<V, DCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
   launch_pdl(tailor_move_kernel<V, DCV>, grid, dim3(256), smem, s, g, jobs, slots, meta, pk, pv, P,                 \
-             (const int32_t*)src_scratch, src_stride, ssm);
+             (const int32_t*)src_scratch, src_stride, ssm, err);
 #define MV_CASE(V)       \
   case V:                \
     MV_LAUNCH(V, 0)      \

@@ -9,6 +9,11 @@
 
 namespace arkv {
 
+// Measurement knobs.  The shipped library reads no environment variable: every knob
+// returns its measured default.  A/B builds (`ARKV_NVCC_FLAGS=-DARKV_TUNING_KNOBS`) read
+// the named variable instead; none of them changes results, only launch shapes.
+int tuning_knob(const char* name, int def);
+
 constexpr int kMaxJobs = 96;  // tailor jobs per launch (kernel-parameter array)
 
 // One unit's tailor (Eq. 10) in a wave: sources -> a fresh slot.
@@ -40,7 +45,7 @@ struct TailorJobs {
 int launch_prefill_begin(const Geom& g, const uint16_t* q_win, const uint16_t* k, int P, float* partials,
                          int n_chunks1, float2* acc_pf, double* colsum, cudaStream_t s);
 int launch_prefill_finish(const Geom& g, const double* colsum, int P, double* stats, double* oq, const double* tau,
-                          double stat_eps, cudaStream_t s);
+                          double stat_eps, int32_t* err, cudaStream_t s);
 
 // Tailor of a wave of jobs (D4-D6).
 // Layer-shared states (NEXT-3): the scores of a tailor come either from this cache's KV
@@ -80,6 +85,8 @@ struct DecodeArgs {
   int prefetch;       // fast kernel: items prefetched into L2 ahead of the shared-memory ring
   int item_order;     // fast kernel: 0 Original tiles first; 1 Quantized groups first on odd
                       // (split + unit) CTAs; 2 Quantized groups first everywhere
+  int l2_hints;       // fast kernels: cache tiles stream with L2 evict_first (HH logits and
+                      // accumulators are kept with evict_last either way)
   void* out;
   int out_fp32;
   int32_t* err;

@@ -41,6 +41,23 @@ def sequence_group_ranks(batch: int, world: int, rank: int):
     return list(range(base, base + rps))
 
 
+def sequence_group(batch: int, world: int, rank: int):
+    """The process group of the ranks sharing this rank's sequence (C1), or None when the
+    rank holds whole sequences.  Every rank creates every group, in the same order
+    (torch.distributed.new_group is collective)."""
+    import torch.distributed as dist
+    if world <= batch:
+        return None
+    mine = None
+    rps = world // batch
+    for r0 in range(0, world, rps):
+        ranks = list(range(r0, r0 + rps))
+        g = dist.new_group(ranks)
+        if rank in ranks:
+            mine = g
+    return mine
+
+
 def prefill_sharded(cache, q_win, k, v, group=None, rho_override=None):
     """Prefill of a KV-head shard: local passes + column sums, C1 all-reduce over the
     ranks sharing the sequences, then moments / rho / ingest / tailor."""

@@ -12,7 +12,7 @@ for TOOL in memcheck synccheck racecheck initcheck; do
   grep -E "ERROR SUMMARY|passed|failed" gpurun_out/san/$TOOL.log | tail -3 | tee -a gpurun_out/san/summary.txt
 done
 # synccheck with the mma.sync prefill instead of the tcgen05 one (tool coverage of tcgen05)
-ARKV_PREFILL_TC=0 timeout 900 compute-sanitizer --tool synccheck --print-limit 20 --error-exitcode 9 \
+ARKV_PREFILL_MMA=1 timeout 900 compute-sanitizer --tool synccheck --print-limit 20 --error-exitcode 9 \
    python -m pytest tests/test_parity_gpu.py -q -p no:randomly -m gpu -k "sharded_prefill" > gpurun_out/san/synccheck_notc.log 2>&1
-echo "synccheck (ARKV_PREFILL_TC=0, sharded_prefill) exit=$?" | tee -a gpurun_out/san/summary.txt
+echo "synccheck (ARKV_PREFILL_MMA=1, sharded_prefill) exit=$?" | tee -a gpurun_out/san/summary.txt
 grep -E "ERROR SUMMARY|passed|failed" gpurun_out/san/synccheck_notc.log | tail -3 | tee -a gpurun_out/san/summary.txt

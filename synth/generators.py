@@ -239,3 +239,88 @@ def decode_inputs_margin_fast(sh: Shape, step: int, seed: int = 0, device="cpu")
     v = torch.randn(B, L, Hkv, d, generator=g, device=device)
     v[..., :2] *= 8.0
     return q.to(torch.bfloat16), k.to(torch.bfloat16), v.to(torch.bfloat16)
+
+
+# ---------------------------------------------------------------------------------------
+# "lattice" recipe: a score margin at ANY prompt length (full-size parity, n_e up to 131K).
+#
+# Every key carries an integer level L_j in binary in dims 0..17 (bits 0/1, bf16-exact);
+# the other dims are random bits, with a fixed 0 and 1 in every 32-dim block (dims 18, 19
+# in the first) so every quantization group has min 0 and max 1.  Every query of layer l is
+# q[m] = 2^(m - e_l) for m < 18, else 0 (the same for all heads, window rows and steps).
+# So q.k_j = 2^-e_l * L_j EXACTLY in fp32 and fp64 (integer sums of powers of two), and
+# it stays a common multiple (1 + eps, |eps| < 1e-7) of L_j after the exact-code group
+# quantization of {0, 1} values (int2/4/8 asymmetric: codes 0 / 2^b - 1; fp8: 0 / 448).
+# Attention weights are then exp(c L_j) / Z with c = 2^-e_l / sqrt(d): adjacent levels
+# give heavy-hitter scores a relative gap >= c (>= 2e-5 here), far above fp32 rounding,
+# while bitwise-equal keys (3 % duplicated prompt keys, repeated decode levels) tie
+# EXACTLY in both implementations and exercise the position tie-break.  Prompt levels
+# are 2 * (a permutation of 0..P-1); decode keys take odd levels 2 * randint(P) + 1.
+# e_l = e0 + (l mod 4) with e0 = ceil(log2(2 P / (80 sqrt(d)))): the level range spans
+# <= 80 nats, and rho differs by layer.  Values: N(0, 1) with two x8 outlier channels.
+# ---------------------------------------------------------------------------------------
+LATTICE_BITS = 18
+
+
+def lattice_exponent(sh: Shape, layer: int) -> int:
+    e0 = max(0, math.ceil(math.log2(2 * sh.prompt_len / (80.0 * math.sqrt(sh.head_dim)))))
+    return e0 + (layer % 4)
+
+
+def _lattice_keys(lev: torch.Tensor, d: int, g: torch.Generator, device) -> torch.Tensor:
+    n = lev.shape[0]
+    k = torch.randint(0, 2, (n, d), generator=g, device=device, dtype=torch.int64)
+    bits = torch.arange(LATTICE_BITS, device=device)
+    k[:, :LATTICE_BITS] = (lev[:, None] >> bits[None, :]) & 1
+    k[:, LATTICE_BITS] = 0
+    k[:, LATTICE_BITS + 1] = 1
+    for blk in range(32, d, 32):
+        k[:, blk] = 0
+        k[:, blk + 1] = 1
+    return k.to(torch.bfloat16)
+
+
+def _lattice_query(sh: Shape, layer: int, device) -> torch.Tensor:
+    e = lattice_exponent(sh, layer)
+    q = torch.zeros(sh.head_dim, device=device)
+    q[:LATTICE_BITS] = torch.pow(2.0, torch.arange(LATTICE_BITS, device=device, dtype=torch.float32) - e)
+    return q.to(torch.bfloat16)
+
+
+def prefill_inputs_lattice(sh: Shape, seed: int = 0, device="cpu"):
+    """Lattice recipe (above): q_win [B][L][H_q][W][d], k, v [B][L][H_kv][P][d] bf16."""
+    B, L, Hq, Hkv, d, P, W = (sh.batch, sh.n_layers, sh.n_q_heads, sh.n_kv_heads, sh.head_dim,
+                              sh.prompt_len, sh.window)
+    assert d >= 64 and d % 32 == 0 and 2 * P <= (1 << LATTICE_BITS)
+    qw = torch.empty(B, L, Hq, W, d, dtype=torch.bfloat16, device=device)
+    k = torch.empty(B, L, Hkv, P, d, dtype=torch.bfloat16, device=device)
+    v = torch.empty(B, L, Hkv, P, d, dtype=torch.bfloat16, device=device)
+    idx = torch.arange(P, device=device)
+    for b in range(B):
+        for l in range(L):
+            g = _gen(seed, 9, b, l, device=device)
+            for h in range(Hkv):
+                lev = 2 * torch.randperm(P, generator=g, device=device)
+                dup = torch.rand(P, generator=g, device=device) < 0.03
+                lev = lev[torch.where(dup & (idx > 0), idx - 1, idx)]
+                kk = _lattice_keys(lev, d, g, device)
+                kk[1:][dup[1:]] = kk[:-1][dup[1:]]        # duplicated keys: bitwise copies
+                k[b, l, h] = kk
+            vv = torch.randn(Hkv, P, d, generator=g, device=device)
+            vv[..., :2] *= 8.0
+            v[b, l] = vv.to(torch.bfloat16)
+            qw[b, l] = _lattice_query(sh, l, device)[None, None, :].expand(Hq, W, d)
+    return qw, k, v
+
+
+def decode_inputs_lattice(sh: Shape, step: int, seed: int = 0, device="cpu"):
+    """Lattice recipe decode inputs: q as in the prefill window; new key at an odd level."""
+    B, L, Hq, Hkv, d, P = sh.batch, sh.n_layers, sh.n_q_heads, sh.n_kv_heads, sh.head_dim, sh.prompt_len
+    g = _gen(seed, 10, step, device=device)
+    lev = 2 * torch.randint(0, P, (B * L * Hkv,), generator=g, device=device) + 1
+    k = _lattice_keys(lev, d, g, device).view(B, L, Hkv, d)
+    q = torch.stack([_lattice_query(sh, l, device) for l in range(L)])       # [L][d]
+    q = q[None, :, None, :].expand(B, L, Hq, d).contiguous()
+    v = torch.randn(B, L, Hkv, d, generator=g, device=device)
+    v[..., :2] *= 8.0
+    return q, k, v.to(torch.bfloat16)

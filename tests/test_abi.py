@@ -131,8 +131,8 @@ def test_host_oq_score_equals_oracle(p):
 
 @pytest.mark.parametrize("d,bits,g,layout", [
     (16, 4, 16, 1), (16, 2, 16, 1), (16, 8, 8, 1), (32, 4, 32, 2), (64, 4, 32, 2), (128, 4, 128, 2),
-    (128, 4, 64, 2), (128, 4, 32, 2), (128, 2, 32, 1), (128, 8, 128, 1), (256, 4, 128, 2), (48, 4, 16, 1),
-    (128, 8, 128, 2), (128, 8, 16, 2), (64, 8, 32, 2), (256, 8, 64, 2)])
+    (128, 4, 64, 2), (128, 4, 32, 2), (128, 2, 32, 1), (128, 8, 128, 1), (64, 4, 16, 1), (32, 2, 8, 1),
+    (128, 8, 128, 2), (128, 8, 16, 2), (64, 8, 32, 2), (32, 8, 32, 2)])
 def test_tile_layouts_are_bijections(d, bits, g, layout):
     """PLAIN and FRAG tile layouts: element -> byte maps are bijections covering the tile,
     and the code-slot inverse used by the tailor's packing pass inverts them."""
@@ -141,6 +141,16 @@ def test_tile_layouts_are_bijections(d, bits, g, layout):
                       max_positions=256, quant_mode=mode)
     n = A.arkv_layout_check(c)
     assert n == 32 * d * 2 + 32 * d * 2 + 32 * 4 * (d // g)
+
+
+@pytest.mark.parametrize("d", [48, 80, 96, 160, 192, 256])
+def test_unsupported_head_dims_rejected(d):
+    """Only head dims every kernel path covers (prefill passes, both decode kernels, both
+    move kernels) are accepted: others fail at configuration, never mid-tailor."""
+    c = A.make_config(1, 4, 2, d, window=8, budget_tokens=64, group_size=16, max_positions=256)
+    with pytest.raises(A.ArkvError) as e:
+        A.arkv_cache_bytes(c)
+    assert e.value.code == -2
 
 
 @settings(max_examples=300, deadline=None)

@@ -79,6 +79,13 @@ def run_parity(sh: Shape, budget, steps, seed=0, recipe="margin", rho=None, chec
     if mutate is not None:
         mutate(qw, k, v)
     stats, oq, rho_gpu = gpu.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda(), rho_override=rho)
+    if rho is None:
+        # Eqs. 3-7 first (H, V, K, q_l and rho within 1e-4 of the oracle's own statistics);
+        # only then is the GPU's rho passed through, so both sides start from the same counts
+        st_o, oq_o, rho_o, _ = O.prefill_stats(_np(qw), _np(k), ocfg)
+        np.testing.assert_allclose(stats.cpu().numpy(), st_o, rtol=STAT_RTOL, err_msg="H, V, K")
+        np.testing.assert_allclose(oq.cpu().numpy(), oq_o, rtol=STAT_RTOL, err_msg="q_l")
+        np.testing.assert_allclose(rho_gpu, rho_o, rtol=STAT_RTOL, err_msg="rho")
     ora.prefill(_np(qw), _np(k), _np(v), rho_override=rho_gpu)
     gpu.arkv_check()
     for b in range(sh.batch):
@@ -268,6 +275,40 @@ def test_decode_errors():
     assert rc == -5
 
 
+@pytest.mark.parametrize("kernel", [1, 2, 3])
+def test_nonfinite_inputs_raise(kernel):
+    """SPEC S:329 ("non-finite input -> numeric error"): a NaN / Inf in a decode step's q,
+    k or v, in a prompt row that enters the cache, or in q_win / K (reaching the Eq. 3
+    column sums) is reported by arkv_check as ARKV_ERR_DEVICE; clean calls check OK.
+    Generic (1), split-K (2) and persistent (3) decode kernels."""
+    from paper_2603_08727_b200 import arkv as A
+
+    def expect_device_error(gpu):
+        with pytest.raises(A.ArkvError) as e:
+            gpu.arkv_check()
+        assert e.value.code == -7
+
+    qw, k, v = prefill_inputs(MID, seed=5)
+    gpu, _, _ = make_pair(MID, budget=512, steps=8, decode_kernel=kernel)
+    gpu.arkv_prefill_stats(qw.cuda(), k.cuda(), v.cuda())
+    gpu.arkv_check()
+    q, kn, vn = [t.cuda() for t in decode_inputs(MID, 0, seed=5)]
+    gpu.arkv_decode_step(q, kn, vn)
+    gpu.arkv_check()
+    for which, val in ((2, float("nan")), (0, float("inf")), (1, float("-inf"))):
+        t = [x.clone() for x in decode_inputs(MID, 1 + which, seed=5)]
+        t[which].view(-1)[t[which].numel() - 3] = val       # last unit of the call (layer 1)
+        gpu.arkv_decode_step(*[x.cuda() for x in t])
+        expect_device_error(gpu)
+    # prompt: an Inf in a window row's V (always kept Original), then a NaN in K
+    for tensor, idx in (("v", (0, 1, 0, MID.prompt_len - 1, 7)), ("k", (0, 0, 1, 100, 3))):
+        qw2, k2, v2 = qw.clone(), k.clone(), v.clone()
+        (v2 if tensor == "v" else k2)[idx] = float("inf") if tensor == "v" else float("nan")
+        gpu2, _, _ = make_pair(MID, budget=512, steps=8, decode_kernel=kernel)
+        gpu2.arkv_prefill_stats(qw2.cuda(), k2.cuda(), v2.cuda(), rho_override=[[1.0, 0.5]])
+        expect_device_error(gpu2)
+
+
 def test_determinism_bitwise():
     outs = []
     for _ in range(2):
@@ -320,80 +361,59 @@ def test_sharded_prefill_c1_equals_full():
 
 def test_full_size_configs1_sampled_units():
     """configs[1] at full size, launched exactly as bench.py does (32 layers x 8 KV heads
-    in one arkv_decode_step per step, default kernel and split count): the oracle
-    recomputes sampled units one by one (two layers with different rho, two KV heads
-    each) through the prefill-end tailor, the HH window and the first decode tailor."""
-    from paper_2603_08727_b200 import arkv as A
-    from synth import prefill_inputs_margin_fast, decode_inputs_margin_fast
+    in one arkv_decode_step per step, default kernel and split count), lattice recipe (a
+    score margin at any size, synth/generators.py): the oracle recomputes two sampled layers
+    (different rho) one unit at a time through the prefill-end tailor (32,736 eligible
+    tokens), the HH window and the first decode tailor.  Every KV head of both layers is
+    compared bit-exactly — no unit is skipped."""
     sh = Shape(batch=1, n_layers=32, n_q_heads=32, n_kv_heads=8, head_dim=128, prompt_len=32768, window=32)
-    steps = 40
-    cfg = A.make_config(32, 32, 8, 128, budget_tokens=8192, max_positions=32768 + steps + 1, max_prompt=32768)
+    checked, oras = _sampled_units_run(sh, 8192, 40, seqs=[0], layers=[3, 16], recipe="lattice", seed=23,
+                                       check_after_prefill=True)
+    assert checked == 2 * 8
+    assert all(len(u.tailors) >= 2 for o in oras.values() for u in o.units.values())   # prefill + decode
+
+
+def test_full_size_configs1_statistics():
+    """Eqs. 3-7 at configs[1]'s full size (P = 32768, all 32 layers, natural recipe): H, V,
+    K, q_l and rho of the CUDA prefill within 1e-4 relative of the float64 oracle's."""
+    from paper_2603_08727_b200 import arkv as A
+    from synth import prefill_inputs_fast
+    sh = Shape(batch=1, n_layers=32, n_q_heads=32, n_kv_heads=8, head_dim=128, prompt_len=32768, window=32)
+    cfg = A.make_config(32, 32, 8, 128, budget_tokens=8192, max_positions=32768 + 2, max_prompt=32768)
     gpu = A.ArkvCache(cfg)
-    qw, k, v = prefill_inputs_margin_fast(sh, seed=23, device="cuda")
+    qw, k, v = prefill_inputs_fast(sh, seed=1234, device="cuda")
     stats, oq, rho = gpu.arkv_prefill_stats(qw, k, v)
     gpu.arkv_check()
-    order = np.argsort(rho[0])
-    layers = [int(order[0]), int(order[len(order) // 2])]       # most quantised + median layer
-    ocfg = O.Cfg(n_layers=1, n_q_heads=32, n_kv_heads=8, head_dim=128, window=32, budget_tokens=8192)
-    oras = {}
-    for l in layers:
-        ora = O.OracleARKV(ocfg)
-        sub = lambda t: t[:, l:l + 1].double().cpu().numpy()   # noqa: E731
-        ora.prefill(sub(qw), sub(k), sub(v), rho_override=[[rho[0, l]]])
-        oras[l] = ora
-    del qw, k, v
-    for l in layers:
-        for h in range(8):
-            e, r = gpu.arkv_export_unit(0, l, h), oras[l].export(0, 0, h)
-            assert (e["n_o"], e["n_q"]) == (r["n_o"], r["n_q"])
-            if min(oras[l].units[(0, 0, h)].margins) <= MARGIN:
-                continue
-            np.testing.assert_array_equal(e["state"], r["state"])
-            qm = r["state"] == 2
-            np.testing.assert_array_equal(e["q_k"][qm], r["q_k"][qm])
-            np.testing.assert_array_equal(e["v_scale"][qm], r["v_scale"][qm])
-    for s in range(steps):
-        q, kn, vn = decode_inputs_margin_fast(sh, s, seed=23, device="cuda")
-        out = gpu.arkv_decode_step(q, kn, vn, out_fp32=True).cpu().numpy()
-        for l in layers:
-            ref = oras[l].decode_step(q[:, l:l + 1].double().cpu().numpy(), kn[:, l:l + 1].double().cpu().numpy(),
-                                      vn[:, l:l + 1].double().cpu().numpy())
-            np.testing.assert_allclose(out[:, l:l + 1], ref, rtol=RTOL, atol=ATOL, err_msg=f"layer {l} step {s}")
-    gpu.arkv_check()
-    for l in layers:
-        assert len(oras[l].units[(0, 0, 0)].tailors) >= 2       # prefill-end + first decode tailor
-        full = 0
-        for h in range(8):
-            e, r = gpu.arkv_export_unit(0, l, h), oras[l].export(0, 0, h)
-            assert (e["n_o"], e["n_q"]) == (r["n_o"], r["n_q"])
-            margins = oras[l].units[(0, 0, h)].margins
-            if min(margins) <= MARGIN:
-                continue      # a near-tie at a rank threshold: fp32 vs fp64 may rank it differently
-            full += 1
-            np.testing.assert_array_equal(e["state"], r["state"])
-            om, qm = r["state"] == 1, r["state"] == 2
-            np.testing.assert_array_equal(_bf16_bits_to_f64(e["o_v"])[om], r["o_v"][om])
-            np.testing.assert_array_equal(e["q_k"][qm], r["q_k"][qm])
-            np.testing.assert_array_equal(e["k_zero"][qm], r["k_zero"][qm])
-        assert full >= 2, f"layer {l}: fewer than two units with a score margin"
+    ocfg = O.Cfg(n_layers=32, n_q_heads=32, n_kv_heads=8, head_dim=128, window=32, budget_tokens=8192)
+    rs, roq, rrho, _ = O.prefill_stats(qw.double().cpu().numpy(), k.double().cpu().numpy(), ocfg)
+    np.testing.assert_allclose(stats.cpu().numpy(), rs, rtol=STAT_RTOL, err_msg="H, V, K")
+    np.testing.assert_allclose(oq.cpu().numpy(), roq, rtol=STAT_RTOL, err_msg="q_l")
+    np.testing.assert_allclose(rho, rrho, rtol=STAT_RTOL, err_msg="rho")
+    assert rho.min() < 0.5 < rho.max() == 1.0      # the layers differ (the bench's workload)
 
 
-def _sampled_units_run(sh, budget, steps, seqs, layers, recipe, seed, decode_kernel=0):
+def _sampled_units_run(sh, budget, steps, seqs, layers, recipe, seed, decode_kernel=0, check_after_prefill=False,
+                       quant="asym", out_fp32=True):
     """Run a full-size cache for `steps` decode steps (bench launch: one call for all
-    layers) and compare sampled (sequence, layer) slices with per-slice oracles."""
+    layers) and compare sampled (sequence, layer) slices with per-slice oracles: outputs
+    every step; counts, states, codes, scales and Original values of every sampled unit
+    at the end (and after the prefill if asked).  The lattice recipe guarantees a score
+    margin at every rank threshold, which the oracle asserts (no unit is skipped)."""
     from paper_2603_08727_b200 import arkv as A
-    from synth import prefill_inputs_fast, decode_inputs_fast, prefill_inputs_margin_fast, decode_inputs_margin_fast
-    pf = prefill_inputs_margin_fast if recipe == "margin" else prefill_inputs_fast
-    df = decode_inputs_margin_fast if recipe == "margin" else decode_inputs_fast
+    from synth import (prefill_inputs_fast, decode_inputs_fast, prefill_inputs_lattice, decode_inputs_lattice)
+    pf = prefill_inputs_lattice if recipe == "lattice" else prefill_inputs_fast
+    df = decode_inputs_lattice if recipe == "lattice" else decode_inputs_fast
+    bits = 8 if quant == "fp8" else 4
     cfg = A.make_config(sh.n_layers, sh.n_q_heads, sh.n_kv_heads, sh.head_dim, batch=sh.batch, window=sh.window,
                         budget_tokens=budget, max_positions=sh.prompt_len + steps + 1, max_prompt=sh.prompt_len,
-                        decode_kernel=decode_kernel)
+                        decode_kernel=decode_kernel, quant_bits=bits,
+                        quant_mode=A.QUANT_FP8 if quant == "fp8" else A.QUANT_ASYM)
     gpu = A.ArkvCache(cfg)
     qw, k, v = pf(sh, seed=seed, device="cuda")
     stats, oq, rho = gpu.arkv_prefill_stats(qw, k, v)
     gpu.arkv_check()
     ocfg = O.Cfg(n_layers=1, n_q_heads=sh.n_q_heads, n_kv_heads=sh.n_kv_heads, head_dim=sh.head_dim,
-                 window=sh.window, budget_tokens=budget)
+                 window=sh.window, budget_tokens=budget, quant_bits=bits, quant_mode=quant)
     oras = {}
     for b in seqs:
         for l in layers:
@@ -402,29 +422,51 @@ def _sampled_units_run(sh, budget, steps, seqs, layers, recipe, seed, decode_ker
             ora.prefill(sub(qw), sub(k), sub(v), rho_override=[[rho[b, l]]])
             oras[(b, l)] = ora
     del qw, k, v
+
+    def compare_all(where):
+        n = 0
+        for (b, l), ora in oras.items():
+            for h in range(sh.n_kv_heads):
+                margins = ora.units[(0, 0, h)].margins
+                if recipe == "lattice":
+                    assert not margins or min(margins) > MARGIN, f"{where}: lattice input without a margin"
+                elif margins and min(margins) <= MARGIN:
+                    continue   # natural recipe: a near-tie may rank differently in fp32 and fp64
+                _compare_export(gpu, ora, b, l, h, where)
+                n += 1
+        return n
+
+    if check_after_prefill:
+        compare_all("after prefill")
     for s in range(steps):
         q, kn, vn = df(sh, s, seed=seed, device="cuda")
-        out = gpu.arkv_decode_step(q, kn, vn, out_fp32=True).cpu().numpy()
+        out = gpu.arkv_decode_step(q, kn, vn, out_fp32=out_fp32).float().cpu().numpy()
         for (b, l), ora in oras.items():
             ref = ora.decode_step(q[b:b + 1, l:l + 1].double().cpu().numpy(), kn[b:b + 1, l:l + 1].double().cpu().numpy(),
                                   vn[b:b + 1, l:l + 1].double().cpu().numpy())
-            np.testing.assert_allclose(out[b:b + 1, l:l + 1], ref, rtol=RTOL, atol=ATOL, err_msg=f"b{b} l{l} step {s}")
+            if not out_fp32:   # bf16 outputs: the oracle's value rounded to bf16, plus one bf16 ulp
+                ref16 = torch.tensor(ref).to(torch.bfloat16).double().numpy()
+                np.testing.assert_allclose(out[b:b + 1, l:l + 1], ref16, rtol=RTOL + 2.0 ** -8, atol=ATOL,
+                                           err_msg=f"b{b} l{l} step {s} (bf16 out)")
+            else:
+                np.testing.assert_allclose(out[b:b + 1, l:l + 1], ref, rtol=RTOL, atol=ATOL,
+                                           err_msg=f"b{b} l{l} step {s}")
     gpu.arkv_check()
-    checked = 0
-    for (b, l), ora in oras.items():
-        for h in range(sh.n_kv_heads):
-            e, r = gpu.arkv_export_unit(b, l, h), ora.export(0, 0, h)
-            assert (e["n_o"], e["n_q"]) == (r["n_o"], r["n_q"])
-            margins = ora.units[(0, 0, h)].margins
-            if margins and min(margins) <= MARGIN:
-                continue
-            checked += 1
-            np.testing.assert_array_equal(e["state"], r["state"])
-            om, qm = r["state"] == 1, r["state"] == 2
-            np.testing.assert_array_equal(_bf16_bits_to_f64(e["o_v"])[om], r["o_v"][om])
-            np.testing.assert_array_equal(e["q_k"][qm], r["q_k"][qm])
-            np.testing.assert_array_equal(e["v_scale"][qm], r["v_scale"][qm])
-    return checked, oras
+    return compare_all(f"after {steps} steps"), oras
+
+
+def _compare_export(gpu, ora, b, l, h, where):
+    """Export of GPU unit (b, l, h) vs the oracle's (0, 0, h) slice: counts, states, codes,
+    fp32 scales/zeros, Original bf16 values, bit-exact."""
+    e, r = gpu.arkv_export_unit(b, l, h), ora.export(0, 0, h)
+    tag = f"{where} unit ({b},{l},{h})"
+    assert (e["n_o"], e["n_q"]) == (r["n_o"], r["n_q"]), tag
+    np.testing.assert_array_equal(e["state"], r["state"], err_msg="states " + tag)
+    om, qm = r["state"] == 1, r["state"] == 2
+    np.testing.assert_array_equal(_bf16_bits_to_f64(e["o_k"])[om], r["o_k"][om], err_msg="O keys " + tag)
+    np.testing.assert_array_equal(_bf16_bits_to_f64(e["o_v"])[om], r["o_v"][om], err_msg="O values " + tag)
+    for key in ("q_k", "q_v", "k_scale", "k_zero", "v_scale", "v_zero"):
+        np.testing.assert_array_equal(e[key][qm], r[key][qm], err_msg=key + " " + tag)
 
 
 @pytest.mark.parametrize("kernel", [2, 3])
@@ -443,9 +485,9 @@ def test_full_size_configs2_batch8(kernel):
     """configs[2]'s per-GPU shard at full size (Qwen3-8B: 36 layers, batch 8, 8K prompts,
     B = 2048): prefill-end tailor on every unit; sampled units vs the oracle."""
     sh = Shape(batch=8, n_layers=36, n_q_heads=32, n_kv_heads=8, head_dim=128, prompt_len=8192, window=32)
-    checked, oras = _sampled_units_run(sh, 2048, 40, seqs=[0, 5], layers=[3, 30], recipe="margin", seed=31,
-                                       decode_kernel=kernel)
-    assert checked >= 8
+    checked, oras = _sampled_units_run(sh, 2048, 40, seqs=[0, 5], layers=[3, 30], recipe="lattice", seed=31,
+                                       decode_kernel=kernel, check_after_prefill=True)
+    assert checked == 2 * 2 * 8
     assert all(len(u.tailors) >= 1 for o in oras.values() for u in o.units.values())
 
 
@@ -592,11 +634,20 @@ def test_full_size_configs4_128k():
     """configs[4]'s per-GPU shard at full size (Llama3-8B shapes, 128K prompt, B = 16384 =
     1/8 of the prompt: the tight-budget long-context regime): prefill-end tailor over
     131,040 eligible tokens per unit and 36 decode steps in the bench launch (one call for
-    all 32 layers); two sampled layers vs the oracle, every KV head."""
+    all 32 layers); two sampled layers vs the oracle, every KV head bit-exact (lattice
+    recipe: a score margin at both rank thresholds of all 16 units)."""
     sh = Shape(batch=1, n_layers=32, n_q_heads=32, n_kv_heads=8, head_dim=128, prompt_len=131072, window=32)
-    checked, oras = _sampled_units_run(sh, 16384, 36, seqs=[0], layers=[2, 21], recipe="margin", seed=37)
-    # outputs of all 16 units are compared every step and their counts always; states,
-    # codes and scales bit-exactly for the units whose rank thresholds have a score margin
-    # (with 131K eligible scores a near-tie at a threshold is common: 7 of 16 here)
-    assert checked >= 6
+    checked, oras = _sampled_units_run(sh, 16384, 36, seqs=[0], layers=[2, 21], recipe="lattice", seed=37)
+    assert checked == 2 * 8
     assert all(len(u.tailors) >= 1 for o in oras.values() for u in o.units.values())
+
+
+def test_full_size_configs1_fp8_bf16_out():
+    """configs[1] at full size with the paper's fp8 e4m3 Q tokens (NEXT-2) and bf16 outputs
+    (what bench.py times): lattice recipe, two sampled layers, every KV head bit-exact;
+    outputs against the oracle's rounded to bf16."""
+    sh = Shape(batch=1, n_layers=32, n_q_heads=32, n_kv_heads=8, head_dim=128, prompt_len=32768, window=32)
+    checked, oras = _sampled_units_run(sh, 8192, 40, seqs=[0], layers=[1, 30], recipe="lattice", seed=43,
+                                       quant="fp8", out_fp32=False)
+    assert checked == 2 * 8
+    assert all(len(u.tailors) >= 2 for o in oras.values() for u in o.units.values())
