@@ -389,7 +389,8 @@ def run_arkv(args, wl):
                    "timed_window": f"decode steps {Wm}..{Wm + K - 1} after the prompt; every window below covers "
                                    f"these steps on a fresh cache",
                    "repeats": args.repeats, "ms_per_step_runs": [m / K for m in ms_runs],
-                   "arkv_env": arkv_env()},
+                   "arkv_env": arkv_env(),
+                   "library": os.environ.get("ARKV_LIBRARY", "paper_2603_08727_b200/libarkv.so")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": tp.get("dram_bytes_per_launch") if tp else None,
@@ -709,6 +710,8 @@ def main():
     ap.add_argument("--no-ceiling", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--allow-tuning-library", action="store_true",
+                    help="measurement only: accept ARKV_LIBRARY (an A/B tuning build); the line says so")
     ap.add_argument("--mode", default="arkv", choices=["arkv", "base", "origin", "quant"],
                     help="arkv (stats-driven rho) or the paper's baselines: base, origin (rho=1), quant (rho=0)")
     ap.add_argument("--prompt-len", type=int, default=0, help="debug: override the workload's prompt length")
@@ -721,7 +724,7 @@ def main():
                     help="Q-token format: int4 g128 asymmetric (default) or fp8 e4m3 per-token scale (NEXT-2)")
     args = ap.parse_args()
     ws, rank, _ = dist_env()
-    if args.impl == "arkv" and "ARKV_LIBRARY" in os.environ:
+    if args.impl == "arkv" and "ARKV_LIBRARY" in os.environ and not args.allow_tuning_library:
         # a measurement build (libarkv_tuning.so) is not the product: no bench line from it
         print(json.dumps({"error": "ARKV_LIBRARY is set: bench.py measures the product libarkv.so only",
                           "arkv_env": arkv_env()}), flush=True)

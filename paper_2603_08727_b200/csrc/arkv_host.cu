@@ -1009,6 +1009,7 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<TailorJob> jobs;
   int max_tiles = 1, acc_rows = 0, n_due = 0;
+  double items_sum = 0.0;
   HhPlan hh;  // (sequence, layer) pairs in their HH window this step (fused combine)
   hh.n = 0;
   bool hh_fit = true;
@@ -1056,6 +1057,8 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
       }
       const int tiles = (c->n_o[bl] + 1 + kTile - 1) / kTile + (c->n_q[bl] + kTile - 1) / kTile;
       max_tiles = std::max(max_tiles, tiles);
+      // split-K work items (one Original tile, or a group of up to 3 Quantized tiles)
+      items_sum += (double)g.Hkv * ((c->n_o[bl] + 1 + kTile - 1) / kTile + ((c->n_q[bl] + kTile - 1) / kTile + 2) / 3);
       // attention: segments read, the token read and appended, q read, out written
       c->step_bytes += (double)g.Hkv * ((double)c->n_o[bl] * g.cost_o + (double)c->n_q[bl] * g.cost_q +
                                         2.0 * g.cost_o + 4.0 * g.G * g.d);
@@ -1082,6 +1085,11 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   const int n_units_call = g.batch * n_layers * g.Hkv;
   const int slots = c->num_sms * (c->fast ? 2 : 4);
   int S = (int)std::lround(2.6 * slots / (double)n_units_call);
+  // ... but no fewer than ~kMinItems work items per CTA: a call with few units (one layer per
+  // call, or one KV head per GPU) would otherwise spread each unit over dozens of CTAs that
+  // spend their time filling and draining the pipeline, and the combine merges as many partials
+  static const int min_items = tuning_knob("ARKV_MIN_ITEMS", 12);
+  S = std::min(S, std::max(1, (int)(items_sum / n_units_call / min_items)));
   S = std::max(1, std::min(S, std::min(c->max_splits, max_tiles)));
   if (const int v = tuning_knob("ARKV_SPLITS", 0); v > 0) S = std::min(v, std::min(c->max_splits, max_tiles));
 

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(256) decode_hh_acc(DecodeArgs a) {
   float a1 = 0.f, a2 = 0.f;
 #pragma unroll
   for (int h = 0; h < G; ++h) {
-    const float p = exp2f(a.logits[((int64_t)u * row_stride + ridx) * G + h] - M[h]) * IL[h];
+    const float p = exp2f(a.logits[((int64_t)u * row_stride + ridx) * G + h] - M[h] - a.pscale) * IL[h];
     a1 += p;
     a2 += p * p;
   }
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const Hh
     float a1 = 0.f, a2 = 0.f;
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-      const float p = exp2f(lg[k][h] - sM[h]) * sIL[h];
+      const float p = exp2f(lg[k][h] - sM[h] - a.pscale) * sIL[h];
       a1 += p;
       a2 += p * p;
     }
@@ -468,6 +468,7 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
     a.item_order = tuning_knob("ARKV_ITEM_ORDER", 1);   // measured: alternating O-first / Q-first CTAs -1.2 %
     a.l2_hints = tuning_knob("ARKV_L2_HINTS", 1);
   }
+  a.pscale = fast ? decode_fast_pscale(g) : 0.f;
   a.out = out;
   a.out_fp32 = out_fp32;
   a.err = err;

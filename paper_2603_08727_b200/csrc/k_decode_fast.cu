@@ -187,6 +187,21 @@ __device__ __forceinline__ void unpack8_raw(uint32_t w, uint32_t (&x)[4]) {
 #define ARKV_PV_RAW 0
 #endif
 constexpr bool kPvRaw = ARKV_PV_RAW != 0;
+// PV on SUBNORMAL codes (round 2): the V codes enter the PV contraction as fp16 subnormals
+// c * 2^-24 (one LOP3 per two codes, as the QK logits already do: no "- 1024", no offset to
+// cancel), and the 2^-24 is absorbed by scaling EVERY probability of the fast kernels by
+// 2^-24: p' = 2^(s - m - 24).  The scale is common to l, Σ p z_v and o of every partial, so
+// it cancels in o / l; the Quantized tiles' P' = p' * (s_v 2^24) keep today's fp16 range, the
+// Original tiles' bf16 P' is just 2^-24 smaller.  Consumers of the merged (M, L) outside the
+// kernel subtract DecodeArgs::pscale (the HH samples, the new token's weight).
+#ifndef ARKV_PV_SUB
+#define ARKV_PV_SUB 1
+#endif
+constexpr bool kPvSub = ARKV_PV_SUB != 0;
+// log2 of 1 / (the probability scale) of the int-code kernels; the fp8 kernels (e4m3 codes
+// convert to NORMAL fp16) keep unscaled probabilities
+template <bool F8>
+constexpr float kPScale = (kPvSub && !F8) ? 24.f : 0.f;
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *(uint32_t*)&v;
@@ -464,7 +479,7 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
           l1 += ksc * acc[gr][hh * 2 + 1] + kz * f.qsum[1][gr];
           // PV runs on the raw magic-number codes (1024 + c for rows g, 1024 + 16c for
           // rows g+8, whose P' carries 1/16): the offset is removed here, in the z term
-          zv[mt][hh][gr] = kPvRaw ? vz - (hh ? 64.f : 1024.f) * vs : vz;
+          zv[mt][hh][gr] = (kPvRaw && !kPvSub) ? vz - (hh ? 64.f : 1024.f) * vs : vz;
         }
         lg[mt][hh * 2 + 0] = l0 * c2;
         lg[mt][hh * 2 + 1] = l1 * c2;
@@ -536,7 +551,7 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float mm = s.m_run[e & 1];
-      p[mt][e] = (mm == -INFINITY) ? 0.f : ex2_ftz(lg[mt][e] - mm);  // ex2(-inf) = 0 for masked rows
+      p[mt][e] = (mm == -INFINITY) ? 0.f : ex2_ftz(lg[mt][e] - (mm + kPScale<F8>));  // ex2(-inf) = 0 for masked rows
       s.l_run[e & 1] += p[mt][e];
     }
 
@@ -581,7 +596,8 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
       for (int gr = 0; gr < NG; ++gr) {
         float pv[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) pv[e] = p[kc][e] * sc[((kc * 16 + gq + 8 * (e >> 1)) * NG + gr) * 4 + 2];
+        for (int e = 0; e < 4; ++e)
+          pv[e] = p[kc][e] * sc[((kc * 16 + gq + 8 * (e >> 1)) * NG + gr) * 4 + 2];
         make_b<G, false>(pv, tq, b01[gr][kc], b23[gr][kc], c01[gr][kc], c23[gr][kc]);
       }
     }
@@ -607,7 +623,8 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
       for (int gr = 0; gr < NG; ++gr) {
         float vsc[2];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) vsc[hh] = sc[((kc * 16 + gq + 8 * hh) * NG + gr) * 4 + 2];
+        for (int hh = 0; hh < 2; ++hh)
+          vsc[hh] = sc[((kc * 16 + gq + 8 * hh) * NG + gr) * 4 + 2] * (kPvSub ? kSubScale : 1.f);
         float pv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) pv[e] = p[kc][e] * vsc[e >> 1] * ((e >> 1) ? 0.0625f : 1.f);
@@ -626,7 +643,10 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
         const int mv = 2 * qd + hm;
         const int gr = (mv * 16) / (D / NG);
         uint32_t x[4], y[4];
-        if (kPvRaw) {
+        if (kPvSub) {
+          unpack8_sub(word(r, 2 * hm + 0), x);  // dim row g: c * 2^-24 (odd tokens 16c * 2^-24)
+          unpack8_sub(word(r, 2 * hm + 1), y);  // dim row g+8
+        } else if (kPvRaw) {
           unpack8_raw(word(r, 2 * hm + 0), x);  // dim row g
           unpack8_raw(word(r, 2 * hm + 1), y);  // dim row g+8
         } else {
@@ -898,7 +918,7 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
       O += ow * cw;
     }
     if (owns_new) {
-      const float cn = exp2f(snew - M);
+      const float cn = exp2f(snew - M - kPScale<F8>);  // the partials' probability scale (kPvSub)
       L += cn;
       O += cn * bf16_to_f(vn[x]);
     }
@@ -1325,7 +1345,7 @@ __global__ void __launch_bounds__(G * D) decode_persist_combine(DecodeArgs a) {
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float L = lane == 0 ? exp2f(s_new[h] - M) : 0.f;
+    float L = lane == 0 ? exp2f(s_new[h] - M - a.pscale) : 0.f;
     for (int k = lane; k < ncand; k += 32) {
       const float* ph = pp + ((int64_t)max(s_slot[k], 0) * G + h) * (D + 2);
       const float l = s_slot[k] >= 0 ? __ldcg(ph + 1) : 0.f;
@@ -1343,7 +1363,7 @@ __global__ void __launch_bounds__(G * D) decode_persist_combine(DecodeArgs a) {
     }
   }
   __syncthreads();
-  float O = exp2f(s_new[h] - sM[h]) * bf16_to_f(vx);
+  float O = exp2f(s_new[h] - sM[h] - a.pscale) * bf16_to_f(vx);
 #pragma unroll 4
   for (int k = 0; k < ncand; ++k) {
     const float w = s_w[k][h];
@@ -1405,6 +1425,10 @@ void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s
 void launch_decode_combine_hh(const DecodeArgs& a, const HhPlan& hp, int max_rows, cudaStream_t s);  // k_decode.cu
 
 // Returns the launches issued, + 100 when the step's HH accumulation ran inside the combine.
+float decode_fast_pscale(const Geom& g) {
+  return g.mode == ARKV_QUANT_FP8 ? fast::kPScale<true> : fast::kPScale<false>;
+}
+
 int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
                        const PersistPlan* plan, const HhPlan* hh, int acc_rows) {
   if (!decode_fast_available(a.g)) return -1;

@@ -85,6 +85,9 @@ struct DecodeArgs {
   int prefetch;       // fast kernel: items prefetched into L2 ahead of the shared-memory ring
   int item_order;     // fast kernel: 0 Original tiles first; 1 Quantized groups first on odd
                       // (split + unit) CTAs; 2 Quantized groups first everywhere
+  float pscale;       // log2 of the scale of the partials' probabilities (fast int-code kernels:
+                      // 24, see k_decode_fast.cu kPvSub; fp8 and generic: 0): HH samples use
+                      // 2^(s - M - pscale) / L
   int l2_hints;       // fast kernels: cache tiles stream with L2 evict_first (HH logits and
                       // accumulators are kept with evict_last either way)
   void* out;
@@ -170,4 +173,6 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 // k_decode_fast.cu: true when the tensor-core decode kernel supports this cache.
 bool decode_fast_available(const Geom& g);
+// k_decode_fast.cu: DecodeArgs::pscale of the fast kernels.
+float decode_fast_pscale(const Geom& g);
 }  // namespace arkv
