@@ -267,6 +267,10 @@ def run_arkv(args, wl):
         dist.init_process_group("nccl", device_id=dev)
     Bg, Hkv_g, L, d = wl["batch"], wl["n_kv_heads"], wl["n_layers"], wl["head_dim"]
     shard = shard_units(Bg, Hkv_g, ws, rank)
+    if args.emulate_shard and ws == 1:
+        # one GPU runs rank 0's shard of an N-GPU partition: its step time predicts the N-GPU
+        # step (the decode loop has no collective); value = the global batch's tokens/s then
+        shard = shard_units(Bg, Hkv_g, args.emulate_shard, 0)
     group = sequence_group(Bg, ws, rank) if ws > 1 else None   # C1: the ranks sharing a sequence
     run = Run(args, wl, shard, dev, group)
     K, Wm = args.steps, args.warmup
@@ -390,7 +394,8 @@ def run_arkv(args, wl):
                                    f"these steps on a fresh cache",
                    "repeats": args.repeats, "ms_per_step_runs": [m / K for m in ms_runs],
                    "arkv_env": arkv_env(),
-                   "library": os.environ.get("ARKV_LIBRARY", "paper_2603_08727_b200/libarkv.so")},
+                   "library": os.environ.get("ARKV_LIBRARY", "paper_2603_08727_b200/libarkv.so"),
+                   "emulated_shard_of": args.emulate_shard or None},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": tp.get("dram_bytes_per_launch") if tp else None,
@@ -710,6 +715,8 @@ def main():
     ap.add_argument("--no-ceiling", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--emulate-shard", type=int, default=0,
+                    help="measurement: on 1 GPU, run rank 0's shard of an N-GPU partition (its step time)")
     ap.add_argument("--allow-tuning-library", action="store_true",
                     help="measurement only: accept ARKV_LIBRARY (an A/B tuning build); the line says so")
     ap.add_argument("--mode", default="arkv", choices=["arkv", "base", "origin", "quant"],

@@ -14,7 +14,10 @@ namespace arkv {
 // the named variable instead; none of them changes results, only launch shapes.
 int tuning_knob(const char* name, int def);
 
-constexpr int kMaxJobs = 96;  // tailor jobs per launch (kernel-parameter array)
+#ifndef ARKV_MAX_JOBS
+#define ARKV_MAX_JOBS 256
+#endif
+constexpr int kMaxJobs = ARKV_MAX_JOBS;  // tailor jobs per launch (kernel-parameter array: 15 KB of the 32 KB limit)
 
 // One unit's tailor (Eq. 10) in a wave: sources -> a fresh slot.
 struct TailorJob {

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Round 2: split-count sweep for small calls (emulated N-GPU shards) and per-layer calls.
+cd $GRAFT_REPO_ROOT
+python -m paper_2603_08727_b200.build --tuning > /dev/null 2>&1
+O=gpurun_out/r2_ssweep; mkdir -p $O
+T=$PWD/paper_2603_08727_b200/libarkv_tuning.so
+B="python bench.py --steps 256 --warmup 8 --repeats 2 --no-cpu-baseline --no-ceiling --no-e2e --no-graph --allow-tuning-library"
+run() { ARKV_LIBRARY=$T ARKV_SPLITS=$2 timeout 600 $B --emulate-shard $1 > $O/n$1_s$2.json 2>$O/n$1_s$2.err
+  python -c "import json; d=json.load(open('$O/n$1_s$2.json')); print('N=$1 S=$2', 'ms/step %.4f' % d['ms_per_step'], 'kernel ms %.4f' % d['roofline']['kernel_ms_per_launch'])" || tail -2 $O/n$1_s$2.err; }
+for s in 4 6 8 9 12 16 18 24; do run 8 $s; done
+for s in 3 4 5 6 8 9 12; do run 4 $s; done
+for s in 2 3 4 5 6; do run 2 $s; done
+G="python bench.py --steps 64 --warmup 8 --repeats 1 --no-cpu-baseline --no-ceiling --no-e2e --allow-tuning-library --graph-steps 64"
+for s in 8 16 18 24 32 37; do
+  ARKV_LIBRARY=$T ARKV_SPLITS=$s timeout 600 $G > $O/layer_s$s.json 2>$O/layer_s$s.err
+  python -c "import json; d=json.load(open('$O/layer_s$s.json')); print('per-layer S=$s', 'graph ms/step %.4f' % d['per_layer_graph']['ms_per_step'])" || tail -2 $O/layer_s$s.err
+done
