@@ -590,7 +590,9 @@ def read_ceiling_gbs(dev) -> float:
 
 def cache_kernel(cache) -> str:
     from paper_2603_08727_b200 import arkv as A
-    return {0: "generic", 1: "fast", 2: "persistent"}[A.lib().arkv_cache_info(cache.handle, 1)]
+    return {0: "generic", 1: "split-K", 2: "persistent",
+            3: "auto (split-K; persistent when >= 60% of a call's bytes are Quantized tiles)"}[
+        A.lib().arkv_cache_info(cache.handle, 1)]
 
 
 def traffic_record(args, kind):

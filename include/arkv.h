@@ -252,7 +252,8 @@ arkv_status arkv_profile_read(arkv_cache* cache, int32_t which, double* total_ms
 
 /* Introspection: what = 0 -> tile layout in use (ARKV_LAYOUT_PLAIN / _FRAG);
    1 -> decode kernel in use (0 generic, 1 tensor-core split-K kernel, 2 tensor-core
-   persistent kernel).  -1 on error. */
+   persistent kernel, 3 auto: split-K, or the persistent kernel for a call whose bytes are
+   mostly Quantized tiles).  -1 on error. */
 int32_t arkv_cache_info(const arkv_cache* cache, int32_t what);
 
 /* Number of kernel launches issued by this cache so far (bench accounting). */

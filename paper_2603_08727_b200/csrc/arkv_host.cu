@@ -559,7 +559,7 @@ int64_t arkv_launch_count(const arkv_cache* c) { return c ? c->launches : 0; }
 int32_t arkv_cache_info(const arkv_cache* c, int32_t what) {
   if (!c) return -1;
   if (what == 0) return c->g.layout;
-  if (what == 1) return c->persist ? 2 : (c->fast ? 1 : 0);
+  if (what == 1) return c->persist ? 2 : (c->fast ? (c->cfg.decode_kernel == 0 ? 3 : 1) : 0);
   return -1;
 }
 
@@ -1009,7 +1009,7 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<TailorJob> jobs;
   int max_tiles = 1, acc_rows = 0, n_due = 0;
-  double items_sum = 0.0;
+  double items_sum = 0.0, seg_o = 0.0, seg_q = 0.0;
   HhPlan hh;  // (sequence, layer) pairs in their HH window this step (fused combine)
   hh.n = 0;
   bool hh_fit = true;
@@ -1062,6 +1062,8 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
       // attention: segments read, the token read and appended, q read, out written
       c->step_bytes += (double)g.Hkv * ((double)c->n_o[bl] * g.cost_o + (double)c->n_q[bl] * g.cost_q +
                                         2.0 * g.cost_o + 4.0 * g.G * g.d);
+      seg_o += (double)c->n_o[bl] * g.cost_o;
+      seg_q += (double)c->n_q[bl] * g.cost_q;
       const int acc0 = acc0_of(g, c->trig[bl], c->q0[bl]);
       if (t >= acc0 && t < c->trig[bl]) {  // HH accumulation step (R19)
         const int rows = c->n_o[bl] + 1 + c->n_q[bl];
@@ -1111,12 +1113,18 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   }
   PlanArgs pa;
   static const bool fuse_hh = tuning_knob("ARKV_FUSE_HH", 1) != 0;
-  if (acc_rows > 0 && hh_fit && fuse_hh && !c->persist) {
+  // auto kernel choice per call: the persistent range-partitioned kernel also when most of
+  // the call's bytes are Quantized tiles (ALU-heavy items: its equal per-CTA ranges beat
+  // split-K's per-unit splits; measured in Base_quant mode: 0.68 vs 0.51 of the copy peak)
+  static const int q_share_pct = tuning_knob("ARKV_PERSIST_QSHARE", 60);
+  const bool persist = c->persist || (c->fast && c->cfg.decode_kernel == 0 &&
+                                      seg_q > 0.01 * q_share_pct * (seg_o + seg_q));
+  if (acc_rows > 0 && hh_fit && fuse_hh && !persist) {
     hh.n_units = g.batch * n_layers * g.Hkv;
     pa.hh = &hh;
   }
   PersistPlan plan;
-  if (c->persist) {
+  if (persist) {
     build_plan(c, layer0, n_layers, 2 * c->num_sms, &plan);
     pa.plan = &plan;
     pa.pparts = c->pparts;

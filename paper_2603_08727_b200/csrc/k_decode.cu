@@ -307,13 +307,17 @@ __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const Hh
     combine_unit<G>(a, u, b, li, kvh, dsc, nullptr, nullptr);
     return;
   }
+  // block -> (entry, chunk of its rows, KV head): binary search of the entry's first chunk
   const int idx = blockIdx.x - hp.n_units;
-  const int per_e = g.Hkv * hp.nchunk;
-  const int4 en = hp.e[idx / per_e];
-  const int kvh = (idx % per_e) / hp.nchunk, chunk = idx % hp.nchunk;
+  const int cg = idx / g.Hkv, kvh = idx - cg * g.Hkv;
+  int lo = 0, hi = hp.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (hp.coff[mid] <= cg) lo = mid; else hi = mid - 1;
+  }
+  const int4 en = hp.e[lo];
   const int R = blockDim.x * kHhRowsPerThread;
-  const int n_rows = en.y, r0 = chunk * R;
-  if (r0 >= n_rows) return;
+  const int n_rows = en.y, r0 = (cg - hp.coff[lo]) * R;
   const int b = en.x / a.n_layers, li = en.x % a.n_layers;
   const int u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
   const bool first = en.z != 0;
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const Hh
     float a1 = 0.f, a2 = 0.f;
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-      const float p = exp2f(lg[k][h] - sM[h] - a.pscale) * sIL[h];
+      const float p = ex2_approx_ftz(lg[k][h] - sM[h] - a.pscale) * sIL[h];  // rel. error < 2^-22
       a1 += p;
       a2 += p * p;
     }
@@ -375,8 +379,11 @@ void launch_decode_combine_hh(const DecodeArgs& a, const HhPlan& hp, int max_row
   HhPlan p = hp;
   const int threads = combine_threads(a.g);
   const int R = threads * kHhRowsPerThread;
-  p.nchunk = std::max(1, (max_rows + R - 1) / R);
-  const dim3 grid(p.n_units + p.n * a.g.Hkv * p.nchunk);
+  (void)max_rows;
+  p.coff[0] = 0;
+  for (int i = 0; i < p.n; ++i) p.coff[i + 1] = p.coff[i] + std::max(1, (p.e[i].y + R - 1) / R);
+  p.n_chunks = p.coff[p.n];
+  const dim3 grid(p.n_units + p.n_chunks * a.g.Hkv);
   switch (a.g.G) {
     case 1: launch_pdl(decode_combine_hh<1>, grid, dim3(threads), 0, s, a, p); break;
     case 2: launch_pdl(decode_combine_hh<2>, grid, dim3(threads), 0, s, a, p); break;

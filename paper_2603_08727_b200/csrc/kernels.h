@@ -133,10 +133,11 @@ constexpr int kMaxHhEntries = 256;
 struct HhPlan {
   int n;           // entries
   int n_units;     // units of the call (= combine blocks)
-  int nchunk;      // row chunks per (entry, KV head)
+  int n_chunks;    // row chunks of all entries (HH blocks = n_chunks x H_kv)
   int pad_;
   int4 e[kMaxHhEntries];  // x = b * n_layers + li; y = rows (n_o after the append + n_q);
                           // z = 1 on the window's first step (acc := sample); w = n_q
+  int coff[kMaxHhEntries + 1];  // first chunk of each entry (its own row count: no empty blocks)
 };
 struct PlanArgs {
   const HhPlan* hh = nullptr;         // fused HH plan (split-K fast kernel), or nullptr
