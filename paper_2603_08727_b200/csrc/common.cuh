@@ -306,6 +306,12 @@ __device__ __forceinline__ bool bf16x2_nonfinite(uint32_t w) {
 __device__ __forceinline__ bool bf16x8_nonfinite(const uint4& v) {
   return bf16x2_nonfinite(v.x) | bf16x2_nonfinite(v.y) | bf16x2_nonfinite(v.z) | bf16x2_nonfinite(v.w);
 }
+// Non-zero iff one of the 8 bf16 values has an all-ones exponent: per word (two halves) the
+// masked exponents + 0x0080 carry into bit 15 exactly for 0x7F80 (3 integer ops per word).
+__device__ __forceinline__ uint32_t bf16x8_expmax_bits(const uint4& v) {
+  const uint32_t m = 0x7F807F80u, c = 0x00800080u, top = 0x80008000u;
+  return (((v.x & m) + c) | ((v.y & m) + c) | ((v.z & m) + c) | ((v.w & m) + c)) & top;
+}
 // One warp checks the step's q rows (n_q elements) and new k/v rows (n_kv elements each).
 __device__ __forceinline__ bool warp_step_nonfinite(const uint16_t* q, int n_q, const uint16_t* k, const uint16_t* v,
                                                     int n_kv, int lane) {

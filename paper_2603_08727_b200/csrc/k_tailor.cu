@@ -407,8 +407,8 @@ __device__ __forceinline__ float read_o(const Geom& g, const uint8_t* tile, int 
 }
 
 template <int VPL, int DC>  // values per lane = ceil(d / 32); DC = compile-time head dim (0: runtime)
-__global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs jobs, uint8_t* slots, uint8_t* meta,
-                                                          const uint16_t* __restrict__ pk,
+__global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs jobs, int n_jobs, uint8_t* slots,
+                                                          uint8_t* meta, const uint16_t* __restrict__ pk,
                                                           const uint16_t* __restrict__ pv, int P,
                                                           const int32_t* __restrict__ src_scratch, int src_stride,
                                                           const float* __restrict__ ssm, int32_t* err) {
@@ -416,12 +416,11 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
   griddep_wait();
   Geom g = g_in;
   if (DC) g.d = DC;  // lets the tile-layout index maps fold their divisions into shifts
-  const TailorJob jb = jobs.j[blockIdx.y];
+  const int jix = job_of_tile(jobs, n_jobs, blockIdx.x);
+  const TailorJob jb = jobs.j[jix];
   const int n_o_new = jb.n_oe + jb.n_win_old;
   const int tiles_o = (n_o_new + kTile - 1) / kTile;
-  const int tiles_q = (jb.n_q_new + kTile - 1) / kTile;
-  int tid = blockIdx.x;
-  if (tid >= tiles_o + tiles_q) return;
+  int tid = blockIdx.x - jobs.tile_off[jix];
   const bool dstQ = tid >= tiles_o;
   if (dstQ) tid -= tiles_o;
   const int tbytes = dstQ ? g.tile_q : g.tile_o;
@@ -430,7 +429,7 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
   for (int i = threadIdx.x * 4; i < zbytes; i += blockDim.x * 4) *(uint32_t*)(tile + i) = 0u;
   __syncthreads();
 
-  const int32_t* src = src_scratch + (int64_t)blockIdx.y * src_stride + (dstQ ? g.cap_o : 0);
+  const int32_t* src = src_scratch + (int64_t)jix * src_stride + (dstQ ? g.cap_o : 0);
   uint8_t* nslot = slots + (int64_t)jb.new_slot * g.slot_bytes;
   const uint8_t* oslot = jb.old_slot >= 0 ? slots + (int64_t)jb.old_slot * g.slot_bytes : nullptr;
   SlotMeta nm = slot_meta(meta, g, jb.new_slot);
@@ -465,7 +464,7 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
       }
       if (ssm) {  // R34: the row's smoothed score at this tailor (read only if it was eligible)
         const int st_stride = max(g.max_pos, g.cap_o) + g.cap_q;
-        const float sc = ssm[(int64_t)blockIdx.y * st_stride + (kind == kSrcOldQ ? st_stride - g.cap_q + orow : orow)];
+        const float sc = ssm[(int64_t)jix * st_stride + (kind == kSrcOldQ ? st_stride - g.cap_q + orow : orow)];
         (dstQ ? nm.sp_q : nm.sp_o)[row] = sc;
       }
     }
@@ -623,7 +622,7 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
                                                                const uint16_t* __restrict__ pv, int P,
                                                                const int32_t* __restrict__ src_scratch,
                                                                int src_stride, const float* __restrict__ ssm,
-                                                               int32_t* err) {
+                                                               int32_t* err, int n_jobs) {
   using namespace mvf;
   __shared__ __align__(16) Smem sm;
   griddep_wait();
@@ -633,15 +632,14 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
   g.ng = NG;
   g.layout = ARKV_LAYOUT_FRAG;
   constexpr int GS = D / NG;  // group size
-  const TailorJob jb = jobs.j[blockIdx.y];
+  const int jix = job_of_tile(jobs, n_jobs, blockIdx.x);
+  const TailorJob jb = jobs.j[jix];
   const int n_o_new = jb.n_oe + jb.n_win_old;
   const int tiles_o = (n_o_new + kTile - 1) / kTile;
-  const int tiles_q = (jb.n_q_new + kTile - 1) / kTile;
-  int tid = blockIdx.x;
-  if (tid >= tiles_o + tiles_q) return;
+  int tid = blockIdx.x - jobs.tile_off[jix];
   const bool dstQ = tid >= tiles_o;
   if (dstQ) tid -= tiles_o;
-  const int32_t* src = src_scratch + (int64_t)blockIdx.y * src_stride + (dstQ ? g.cap_o : 0);
+  const int32_t* src = src_scratch + (int64_t)jix * src_stride + (dstQ ? g.cap_o : 0);
   uint8_t* nslot = slots + (int64_t)jb.new_slot * g.slot_bytes;
   const uint8_t* oslot = jb.old_slot >= 0 ? slots + (int64_t)jb.old_slot * g.slot_bytes : nullptr;
   SlotMeta nm = slot_meta(meta, g, jb.new_slot);
@@ -673,13 +671,13 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
       }
       if (ssm) {  // R34: the row's smoothed score at this tailor (read only if it was eligible)
         const int st_stride = max(g.max_pos, g.cap_o) + g.cap_q;
-        const float sc = ssm[(int64_t)blockIdx.y * st_stride + (kind == kSrcOldQ ? st_stride - g.cap_q + orow : orow)];
+        const float sc = ssm[(int64_t)jix * st_stride + (kind == kSrcOldQ ? st_stride - g.cap_q + orow : orow)];
         (dstQ ? nm.sp_q : nm.sp_o)[row] = sc;
       }
     }
   }
   // ---- phase 1: one warp per row ----
-  bool nonfinite = false;
+  uint32_t nonfinite_bits = 0u;
   for (int j = warp, r = 0; j < kTile; j += 8, ++r) {
     const int row = tid * kTile + j;
     const int32_t sref = __shfl_sync(0xffffffffu, my_sref, r);
@@ -716,7 +714,7 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
       const uint16_t* rowp = (lane < 16 ? upk : upv) + (int64_t)orow * D + (lane & 15) * 8;
       const uint4 pr = *(const uint4*)rowp;
       *(uint4*)&sm.stage[lane >> 4][j][(lane & 15) * 8] = pr;
-      nonfinite |= bf16x8_nonfinite(pr);  // prompt values entering the cache
+      nonfinite_bits |= bf16x8_expmax_bits(pr);  // prompt values entering the cache
     } else {
       // old Original row: K quad (t, q) holds dims 32t + 8q .. +7 of the token (FRAG K map)
       const uint8_t* ot = o_tile_ptr((uint8_t*)oslot, g, orow >> 5);
@@ -788,7 +786,7 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
     }
     if (lane % LPG == 0) sm.sc[j][lane / LPG] = scv;
   }
-  if (nonfinite) atomicOr(err, kErrNonFinite);
+  if (nonfinite_bits) atomicOr(err, kErrNonFinite);
   __syncthreads();
 
   // ---- phase 2: 16-byte output quads straight to HBM ----
@@ -879,18 +877,25 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
              (const float*)shs.sscore, shs.ext, shs.ext_stride, shs.ext_heads, g.smooth > 0.f ? shs.ssm : nullptr);
   launch_pdl(tailor_scan_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, desc, (const int8_t*)st_scratch, st_stride,
              src_scratch, src_stride, err);
-  dim3 grid(max_tiles, n_jobs);
+  // one CTA per destination tile of every job (no idle CTAs for the smaller jobs)
+  TailorJobs mj = jobs;
+  mj.tile_off[0] = 0;
+  for (int k = 0; k < n_jobs; ++k)
+    mj.tile_off[k + 1] = mj.tile_off[k] + (mj.j[k].n_oe + mj.j[k].n_win_old + kTile - 1) / kTile +
+                         (mj.j[k].n_q_new + kTile - 1) / kTile;
+  (void)max_tiles;
+  const dim3 grid(std::max(1, mj.tile_off[n_jobs]));
   const float* ssm = g.smooth > 0.f ? shs.ssm : nullptr;
   if (g.layout == ARKV_LAYOUT_FRAG && g.d == mvf::D && g.bits == 4 && tuning_knob("ARKV_MOVE_GENERIC", 0) == 0) {
     switch (g.ng) {
-      case 1: launch_pdl(tailor_move_frag_kernel<1>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride, ssm, err); return 3 + extra;
-      case 2: launch_pdl(tailor_move_frag_kernel<2>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride, ssm, err); return 3 + extra;
-      case 4: launch_pdl(tailor_move_frag_kernel<4>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride, ssm, err); return 3 + extra;
-      case 8: launch_pdl(tailor_move_frag_kernel<8>, grid, dim3(256), 0, s, g, jobs, slots, meta, pk, pv, P,
-                         (const int32_t*)src_scratch, src_stride, ssm, err); return 3 + extra;
+      case 1: launch_pdl(tailor_move_frag_kernel<1>, grid, dim3(256), 0, s, g, mj, slots, meta, pk, pv, P,
+                         (const int32_t*)src_scratch, src_stride, ssm, err, n_jobs); return 3 + extra;
+      case 2: launch_pdl(tailor_move_frag_kernel<2>, grid, dim3(256), 0, s, g, mj, slots, meta, pk, pv, P,
+                         (const int32_t*)src_scratch, src_stride, ssm, err, n_jobs); return 3 + extra;
+      case 4: launch_pdl(tailor_move_frag_kernel<4>, grid, dim3(256), 0, s, g, mj, slots, meta, pk, pv, P,
+                         (const int32_t*)src_scratch, src_stride, ssm, err, n_jobs); return 3 + extra;
+      case 8: launch_pdl(tailor_move_frag_kernel<8>, grid, dim3(256), 0, s, g, mj, slots, meta, pk, pv, P,
+                         (const int32_t*)src_scratch, src_stride, ssm, err, n_jobs); return 3 + extra;
       default: break;
     }
   }
@@ -898,7 +903,7 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
   const int vpl = (g.d + 31) / 32;
 #define MV_LAUNCH(V, DCV)                                                                                         \
   cudaFuncSetAttribute(tailor_move_kernel<V, DCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
-  launch_pdl(tailor_move_kernel<V, DCV>, grid, dim3(256), smem, s, g, jobs, slots, meta, pk, pv, P,                 \
+  launch_pdl(tailor_move_kernel<V, DCV>, grid, dim3(256), smem, s, g, mj, n_jobs, slots, meta, pk, pv, P,         \
              (const int32_t*)src_scratch, src_stride, ssm, err);
 #define MV_CASE(V)       \
   case V:                \

@@ -41,7 +41,18 @@ struct TailorJob {
 };
 struct TailorJobs {
   TailorJob j[kMaxJobs];
+  int32_t tile_off[kMaxJobs + 1];  // move kernels: first destination tile of each job (a 1-D
+                                   // grid of exactly the jobs' tiles; filled by launch_tailor)
 };
+// job of destination tile `t` of a move launch (binary search of tile_off)
+__device__ __forceinline__ int job_of_tile(const TailorJobs& jobs, int n_jobs, int t) {
+  int lo = 0, hi = n_jobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (jobs.tile_off[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
 
 // Prefill statistics: passes 1-2 + local Eq. 3 column sums; then the
 // moments / OQ score from (possibly all-reduced) column sums.  Return launches.
