@@ -294,8 +294,7 @@ static int combine_threads(const Geom& g) { return std::min(1024, std::max(128, 
 // decode_hh_acc launch and its drain).  Combine blocks as decode_combine; an HH block
 // recomputes its unit's merged (M, 1/L) with the combine's own code (bit-identical), then
 // folds rows [chunk * R, chunk * R + R) exactly as decode_hh_acc does.
-constexpr int kHhRowsPerThread = 4;
-template <int G>
+template <int G, int kHhRowsPerThread>
 __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const HhPlan hp) {
   griddep_wait();
   griddep_launch_dependents();
@@ -376,21 +375,30 @@ __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const Hh
 }
 
 void launch_decode_combine_hh(const DecodeArgs& a, const HhPlan& hp, int max_rows, cudaStream_t s) {
+  // 256 threads x 8 rows per HH block (measured against 512 x 4: more rows in flight per
+  // thread, the same 2048 rows per block); the combine blocks loop over their G * d outputs
+  static const int rpt = tuning_knob("ARKV_HH_RPT", 8);
   HhPlan p = hp;
-  const int threads = combine_threads(a.g);
-  const int R = threads * kHhRowsPerThread;
+  const int threads = rpt == 8 ? 256 : combine_threads(a.g);
+  const int R = threads * rpt;
   (void)max_rows;
   p.coff[0] = 0;
   for (int i = 0; i < p.n; ++i) p.coff[i + 1] = p.coff[i] + std::max(1, (p.e[i].y + R - 1) / R);
   p.n_chunks = p.coff[p.n];
   const dim3 grid(p.n_units + p.n_chunks * a.g.Hkv);
+#define HH_CASE(GV)                                                                                          \
+  case GV:                                                                                                   \
+    if (rpt == 8) launch_pdl(decode_combine_hh<GV, 8>, grid, dim3(threads), 0, s, a, p);                     \
+    else launch_pdl(decode_combine_hh<GV, 4>, grid, dim3(threads), 0, s, a, p);                              \
+    break;
   switch (a.g.G) {
-    case 1: launch_pdl(decode_combine_hh<1>, grid, dim3(threads), 0, s, a, p); break;
-    case 2: launch_pdl(decode_combine_hh<2>, grid, dim3(threads), 0, s, a, p); break;
-    case 4: launch_pdl(decode_combine_hh<4>, grid, dim3(threads), 0, s, a, p); break;
-    case 8: launch_pdl(decode_combine_hh<8>, grid, dim3(threads), 0, s, a, p); break;
+    HH_CASE(1)
+    HH_CASE(2)
+    HH_CASE(4)
+    HH_CASE(8)
     default: break;
   }
+#undef HH_CASE
 }
 
 void launch_decode_hh_acc(const DecodeArgs& a, int n_units_call, int max_rows, cudaStream_t s) {
@@ -474,6 +482,12 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
     a.prefetch = tuning_knob("ARKV_PREFETCH", 0);
     a.item_order = tuning_knob("ARKV_ITEM_ORDER", 1);   // measured: alternating O-first / Q-first CTAs -1.2 %
     a.l2_hints = tuning_knob("ARKV_L2_HINTS", 1);
+    a.self_refill = tuning_knob("ARKV_SELF_REFILL", 1);
+#ifdef ARKV_TUNING_KNOBS
+    a.hh_nostore = tuning_knob("ARKV_HH_NOSTORE", 0);  // measurement of the store cost only
+#else
+    a.hh_nostore = 0;
+#endif
   }
   a.pscale = fast ? decode_fast_pscale(g) : 0.f;
   a.out = out;

@@ -756,19 +756,25 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
   }
   __syncthreads();
 
+  auto item_src = [&](int i, const uint8_t*& src, uint32_t& bytes) {
+    bool isq;
+    int first, ntiles;
+    item_of(i, isq, first, ntiles);
+    src = isq ? q_tile_ptr(slot, g, first + ntiles - 1) : o_tile_ptr(slot, g, first);
+    bytes = isq ? (uint32_t)(ntiles * g.tile_q) : (uint32_t)g.tile_o;
+  };
+  // Self-refill (default): each consumer warp's lane 0 loads its own items — the first SPW
+  // at the start, then item i + kStages into the stage it has just consumed.  A slow
+  // (Quantized) item then delays only its own warp's next load; with one in-order producer
+  // every other warp's refill waited behind it (head-of-line blocking), which dominated
+  // calls with few items per CTA (per-layer calls, 8-GPU shards).
+  const bool self_refill = a.self_refill != 0;
   if (warp == kConsumers) {
     // ===================== producer =====================
-    if (lane == 0) {
+    if (lane == 0 && !self_refill) {
       const uint64_t pol_stream = l2_evict_first();
       // items in order (measured: polling stages out of order and busy-waiting costs the
       // co-scheduled consumer warp issue slots; try_wait suspends in hardware)
-      auto item_src = [&](int i, const uint8_t*& src, uint32_t& bytes) {
-        bool isq;
-        int first, ntiles;
-        item_of(i, isq, first, ntiles);
-        src = isq ? q_tile_ptr(slot, g, first + ntiles - 1) : o_tile_ptr(slot, g, first);
-        bytes = isq ? (uint32_t)(ntiles * g.tile_q) : (uint32_t)g.tile_o;
-      };
       const int ahead = a.prefetch;  // items requested into L2 ahead of the ring (0: off)
       for (int i = 0; i < min(ahead, n_work); ++i) {
         const uint8_t* src;
@@ -838,6 +844,21 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
   } else {
     // ===================== consumers =====================
     const uint64_t lpol = l2_evict_last();  // HH logits stay in L2 for the combine
+    const uint64_t pol_stream = l2_evict_first();
+    auto issue = [&](int i) {  // lane 0: item i into its stage (the stage is free)
+      const int st = stage_of(i);
+      const uint8_t* src;
+      uint32_t bytes;
+      item_src(i, src, bytes);
+      mbar_expect_tx(&sm.full[st], bytes);
+      if (a.l2_hints)
+        bulk_g2s_hint(sm.ring[st], src, bytes, &sm.full[st], pol_stream);
+      else
+        bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
+    };
+    if (self_refill && lane == 0)
+      for (int k = 0; k < SPW; ++k)
+        if (warp + k * kConsumers < n_work) issue(warp + k * kConsumers);
     QFrag<NG> qf;
     load_qfrag<G, NG, F8>(qp, lane, qf);
     Acc<NG> acc;
@@ -857,13 +878,23 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
         const uint8_t* tb = sm.ring[st] + (isq ? (ntiles - 1 - jt) * g.tile_q : 0);
         const int tile = first + jt;
         const int n_valid = isq ? min(kTile, n_q - tile * kTile) : min(kTile, n_o - tile * kTile);
-        float* lrow =
-            accm ? a.logits + ((int64_t)u * row_stride + (isq ? g.cap_o : 0) + tile * kTile) * G : nullptr;
+        float* lrow = (accm && !a.hh_nostore)
+                          ? a.logits + ((int64_t)u * row_stride + (isq ? g.cap_o : 0) + tile * kTile) * G
+                          : nullptr;
         consume_tile<G, NG, F8>(tb, isq, n_valid, lrow, row_stride, lpol, qf, acc, c2, sym, lane, src_lane);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[st]);
+      if (self_refill) {
+        if (lane == 0 && i + kStages < n_work) {
+          // this warp's reads of the stage (generic proxy) before the refill (async proxy)
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          issue(i + kStages);
+        }
+      } else if (lane == 0) {
+        mbar_arrive(&sm.empty[st]);
+      }
     }
+    if (self_refill && warp == 0 && lane == 0) griddep_launch_dependents();  // PDL (the combine waits for us)
     // ---- per-warp finalisation: reduce l and z over the 8 row lanes ----
     acc_reduce_rows(acc);
     if (gq == 0) {

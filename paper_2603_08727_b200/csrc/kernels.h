@@ -102,6 +102,8 @@ struct DecodeArgs {
   float pscale;       // log2 of the scale of the partials' probabilities (fast int-code kernels:
                       // 24, see k_decode_fast.cu kPvSub; fp8 and generic: 0): HH samples use
                       // 2^(s - M - pscale) / L
+  int self_refill;    // split kernel: each consumer warp loads its own next item (no in-order producer)
+  int hh_nostore;     // tuning builds only (results wrong): the split kernel skips the HH logit stores
   int l2_hints;       // fast kernels: cache tiles stream with L2 evict_first (HH logits and
                       // accumulators are kept with evict_last either way)
   void* out;
