@@ -605,6 +605,7 @@ __global__ void __launch_bounds__(256) tailor_move_kernel(Geom g_in, TailorJobs 
 // the FRAG maps of common.cuh specialised to d = 128 (no per-element layout arithmetic
 // on the store side).
 // ---------------------------------------------------------------------------------
+constexpr int kMoveTilesPerCta = 4;  // tailor_move_frag_kernel: destination tiles per CTA
 namespace mvf {
 constexpr int D = 128;
 constexpr int kRowH = D + 8;    // staged row stride in bf16 (pad: conflict-free transposed reads)
@@ -632,14 +633,15 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
   g.ng = NG;
   g.layout = ARKV_LAYOUT_FRAG;
   constexpr int GS = D / NG;  // group size
+  // this CTA's destination tiles: kMoveTilesPerCta consecutive tiles of one job (the
+  // per-CTA setup amortised over several tiles; ncu: it was ~25 % of the kernel's
+  // instructions with one tile per CTA)
   const int jix = job_of_tile(jobs, n_jobs, blockIdx.x);
   const TailorJob jb = jobs.j[jix];
   const int n_o_new = jb.n_oe + jb.n_win_old;
   const int tiles_o = (n_o_new + kTile - 1) / kTile;
-  int tid = blockIdx.x - jobs.tile_off[jix];
-  const bool dstQ = tid >= tiles_o;
-  if (dstQ) tid -= tiles_o;
-  const int32_t* src = src_scratch + (int64_t)jix * src_stride + (dstQ ? g.cap_o : 0);
+  const int tiles_all = tiles_o + (jb.n_q_new + kTile - 1) / kTile;
+  const int t_first = (blockIdx.x - jobs.tile_off[jix]) * kMoveTilesPerCta;
   uint8_t* nslot = slots + (int64_t)jb.new_slot * g.slot_bytes;
   const uint8_t* oslot = jb.old_slot >= 0 ? slots + (int64_t)jb.old_slot * g.slot_bytes : nullptr;
   SlotMeta nm = slot_meta(meta, g, jb.new_slot);
@@ -647,9 +649,17 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
   if (jb.old_slot >= 0) om = slot_meta(meta, g, jb.old_slot);
   const uint16_t* upk = pk ? pk + (int64_t)jb.unit * P * D : nullptr;
   const uint16_t* upv = pv ? pv + (int64_t)jb.unit * P * D : nullptr;
-  const int n_new = dstQ ? jb.n_q_new : n_o_new;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int off = g.mode == ARKV_QUANT_SYM ? 8 : 0;
+  uint32_t nonfinite_bits = 0u;
+  for (int rep = 0; rep < kMoveTilesPerCta; ++rep) {
+  int tid = t_first + rep;
+  if (tid >= tiles_all) break;
+  if (rep > 0) __syncthreads();  // the previous tile's phase 2 is done with the staging buffers
+  const bool dstQ = tid >= tiles_o;
+  if (dstQ) tid -= tiles_o;
+  const int32_t* src = src_scratch + (int64_t)jix * src_stride + (dstQ ? g.cap_o : 0);
+  const int n_new = dstQ ? jb.n_q_new : n_o_new;
 
   // ---- phase 0: the source reference and position of the warp's kTile / 8 rows in two
   // batched rounds (lane r < kTile / 8 handles row warp + 8 r) instead of two dependent
@@ -677,7 +687,6 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
     }
   }
   // ---- phase 1: one warp per row ----
-  uint32_t nonfinite_bits = 0u;
   for (int j = warp, r = 0; j < kTile; j += 8, ++r) {
     const int row = tid * kTile + j;
     const int32_t sref = __shfl_sync(0xffffffffu, my_sref, r);
@@ -786,7 +795,6 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
     }
     if (lane % LPG == 0) sm.sc[j][lane / LPG] = scv;
   }
-  if (nonfinite_bits) atomicOr(err, kErrNonFinite);
   __syncthreads();
 
   // ---- phase 2: 16-byte output quads straight to HBM ----
@@ -858,6 +866,8 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
     for (int i = threadIdx.x; i < kTile * NG; i += 256)
       *(float4*)(dst + 32 * D + i * 16) = sm.sc[i / NG][i % NG];
   }
+  }  // rep
+  if (nonfinite_bits) atomicOr(err, kErrNonFinite);
 }
 
 int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_tiles, uint8_t* slots, uint8_t* meta,
@@ -877,16 +887,20 @@ int launch_tailor(const Geom& g, const TailorJobs& jobs, int n_jobs, int max_til
              (const float*)shs.sscore, shs.ext, shs.ext_stride, shs.ext_heads, g.smooth > 0.f ? shs.ssm : nullptr);
   launch_pdl(tailor_scan_kernel, dim3(n_jobs), dim3(1024), 0, s, g, jobs, desc, (const int8_t*)st_scratch, st_stride,
              src_scratch, src_stride, err);
-  // one CTA per destination tile of every job (no idle CTAs for the smaller jobs)
+  // a 1-D grid of exactly the jobs' destination tiles (frag: kMoveTilesPerCta per CTA)
+  const bool frag = g.layout == ARKV_LAYOUT_FRAG && g.d == mvf::D && g.bits == 4 &&
+                    tuning_knob("ARKV_MOVE_GENERIC", 0) == 0;
+  const int tpc = frag ? kMoveTilesPerCta : 1;
   TailorJobs mj = jobs;
   mj.tile_off[0] = 0;
-  for (int k = 0; k < n_jobs; ++k)
-    mj.tile_off[k + 1] = mj.tile_off[k] + (mj.j[k].n_oe + mj.j[k].n_win_old + kTile - 1) / kTile +
-                         (mj.j[k].n_q_new + kTile - 1) / kTile;
+  for (int k = 0; k < n_jobs; ++k) {
+    const int tiles = (mj.j[k].n_oe + mj.j[k].n_win_old + kTile - 1) / kTile + (mj.j[k].n_q_new + kTile - 1) / kTile;
+    mj.tile_off[k + 1] = mj.tile_off[k] + (tiles + tpc - 1) / tpc;
+  }
   (void)max_tiles;
   const dim3 grid(std::max(1, mj.tile_off[n_jobs]));
   const float* ssm = g.smooth > 0.f ? shs.ssm : nullptr;
-  if (g.layout == ARKV_LAYOUT_FRAG && g.d == mvf::D && g.bits == 4 && tuning_knob("ARKV_MOVE_GENERIC", 0) == 0) {
+  if (frag) {
     switch (g.ng) {
       case 1: launch_pdl(tailor_move_frag_kernel<1>, grid, dim3(256), 0, s, g, mj, slots, meta, pk, pv, P,
                          (const int32_t*)src_scratch, src_stride, ssm, err, n_jobs); return 3 + extra;

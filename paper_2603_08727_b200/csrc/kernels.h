@@ -41,8 +41,8 @@ struct TailorJob {
 };
 struct TailorJobs {
   TailorJob j[kMaxJobs];
-  int32_t tile_off[kMaxJobs + 1];  // move kernels: first destination tile of each job (a 1-D
-                                   // grid of exactly the jobs' tiles; filled by launch_tailor)
+  int32_t tile_off[kMaxJobs + 1];  // move kernels: first CTA of each job (a 1-D grid of exactly
+                                   // the jobs' destination tiles; filled by launch_tailor)
 };
 // job of destination tile `t` of a move launch (binary search of tile_off)
 __device__ __forceinline__ int job_of_tile(const TailorJobs& jobs, int n_jobs, int t) {
