@@ -1087,10 +1087,11 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   const int n_units_call = g.batch * n_layers * g.Hkv;
   const int slots = c->num_sms * (c->fast ? 2 : 4);
   int S = (int)std::lround(2.6 * slots / (double)n_units_call);
-  // ... but no fewer than ~kMinItems work items per CTA: a call with few units (one layer per
+  // ... but no fewer than ~20 work items per CTA (sweeps with self-refill: 8-GPU shard S = 12
+  // beats 19, 4-GPU S = 9 beats 12, configs[1] S = 3): a call with few units (one layer per
   // call, or one KV head per GPU) would otherwise spread each unit over dozens of CTAs that
   // spend their time filling and draining the pipeline, and the combine merges as many partials
-  static const int min_items = tuning_knob("ARKV_MIN_ITEMS", 12);
+  static const int min_items = tuning_knob("ARKV_MIN_ITEMS", 20);
   S = std::min(S, std::max(1, (int)(items_sum / n_units_call / min_items)));
   S = std::max(1, std::min(S, std::min(c->max_splits, max_tiles)));
   if (const int v = tuning_knob("ARKV_SPLITS", 0); v > 0) S = std::min(v, std::min(c->max_splits, max_tiles));
