@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <memory>
+#include <numeric>
 #include <vector>
 
 #include "kernels.h"
@@ -56,6 +58,8 @@ struct arkv_cache {
   double* colsum = nullptr;
   float* mstat = nullptr;
   int32_t* counters = nullptr;
+  int32_t* nsplit = nullptr;
+  std::unique_ptr<UnitOrder> chunks{new UnitOrder};  // split-K launch order (host copy, a kernel parameter)
   // persistent decode kernel (decode_kernel = 3): partial slots and coverage tables
   float* pparts = nullptr;
   int4* pcta = nullptr;
@@ -95,7 +99,7 @@ struct Sizes {
   int n_spare, jobs_per_wave, jobs_scratch, max_splits, n_chunks1;
   int64_t arena, ws;
   int64_t off_meta, off_desc, off_err;
-  int64_t w_partials, w_logits, w_st, w_sscore, w_ssm, w_src, w_pfp, w_accpf, w_oq, w_colsum, w_mstat, w_counters, w_plan, w_pparts;
+  int64_t w_partials, w_logits, w_st, w_sscore, w_ssm, w_src, w_pfp, w_accpf, w_oq, w_colsum, w_mstat, w_counters, w_nsplit, w_plan, w_pparts;
 };
 
 int64_t cost_o(const arkv_config& c) { return 4LL * c.head_dim; }
@@ -208,6 +212,8 @@ Sizes compute_sizes(const arkv_config& c) {
   s.w_mstat = w;
   w = round_up(w + (int64_t)g.n_units * g.G * 8, 256);
   s.w_counters = w;
+  w = round_up(w + (int64_t)g.n_units * 4, 256);
+  s.w_nsplit = w;  // split count per unit of a chunk-list decode launch
   w = round_up(w + (int64_t)g.n_units * 4, 256);
   // persistent decode kernel: its plan and one partial per (unit, covering CTA, warp)
   s.w_plan = w;  // pcta [2][kPlanMaxCtas] int4, then pcover [2][2][n_units] int32
@@ -461,6 +467,7 @@ arkv_status arkv_cache_create(const arkv_config* cfg, void* d_arena, size_t aren
   c->colsum = (double*)(w + s.w_colsum);
   c->mstat = (float*)(w + s.w_mstat);
   c->counters = (int32_t*)(w + s.w_counters);
+  c->nsplit = (int32_t*)(w + s.w_nsplit);
   c->pcta = (int4*)(w + s.w_plan);
   c->pcover = (int32_t*)(w + s.w_plan + 2 * kPlanMaxCtas * 16);
   c->pparts = (float*)(w + s.w_pparts);
@@ -998,6 +1005,74 @@ arkv_status arkv_set_tailor_scores(arkv_cache* c, const float* d_scores, int64_t
   return ARKV_OK;
 }
 
+// Cost-balanced split-K launch order (UnitOrder, kernels.h) for the fast decode kernel.
+// Measured (scripts/cta_timeline.py, per-CTA globaltimer stamps at configs[1]): with the same
+// number of splits for every unit, the CTAs of Quantized-heavy units ran 1.8x longer than
+// those of Original-heavy ones (the Quantized path is issue-bound, a 4.5 KB Quantized tile
+// costs ~0.6 of a 16 KB Original tile), and the kernel spent its last 15 % (HH-window steps)
+// with a draining, half-empty grid.  Here a unit's estimated time is its Original tiles +
+// q_cost x its Quantized tiles; the step's CTAs are exactly `waves` x the CTA slots,
+// apportioned to the units by largest remainder of their cost shares (>= 1, <= the
+// per-unit cap of ~min_items work items per CTA and max_splits), and the units are launched
+// in decreasing piece cost (LPT).  Measured at configs[1]: HH-window decode kernel -6 %,
+// steady state -1 % (2 waves beat 3 and 4: fewer per-CTA fills and drains).
+static bool build_chunks(arkv_cache* c, int layer0, int n_layers, int slots) {
+  const Geom& g = c->g;
+  const int n_units = g.batch * n_layers * g.Hkv;
+  static const int mode = tuning_knob("ARKV_CHUNKS", 1);  // 0: the uniform grid
+  if (mode == 0 || n_units > kMaxOrderUnits) return false;
+  static const double q_cost = 0.01 * tuning_knob("ARKV_QCOST", 62);
+  static const int waves = tuning_knob("ARKV_EXACT_WAVES", 2);
+  static const int min_items = tuning_knob("ARKV_MIN_ITEMS", 20);
+  const int BL = g.batch * n_layers;
+  std::vector<double> cost(BL), x(BL);
+  std::vector<int> cap(BL), ns(BL);
+  double total = 0.0;
+  for (int b = 0; b < g.batch; ++b)
+    for (int l = layer0; l < layer0 + n_layers; ++l) {
+      const int bl = b * g.L + l, i = b * n_layers + (l - layer0);
+      const int to = (c->n_o[bl] + 1 + kTile - 1) / kTile, tq = (c->n_q[bl] + kTile - 1) / kTile;
+      cost[i] = to + q_cost * tq;
+      const int items = to + (tq + 2) / 3;
+      cap[i] = std::max(1, std::min({c->max_splits, to + tq, items / std::max(1, min_items), 0xFFFF}));
+      total += cost[i];
+    }
+  // per (sequence, layer): every KV head of it has the same counts and the same split count
+  const int64_t want = std::max<int64_t>(BL, (int64_t)waves * slots / g.Hkv);
+  int64_t n = 0;
+  for (int i = 0; i < BL; ++i) {
+    x[i] = cost[i] / std::max(total, 1e-30) * (double)want;
+    ns[i] = std::max(1, std::min((int)std::floor(x[i]), cap[i]));
+    n += ns[i];
+  }
+  std::vector<int> idx(BL);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int p, int q) { return x[p] - ns[p] > x[q] - ns[q]; });
+  for (int j = 0; j < BL && n < want; ++j)
+    if (ns[idx[j]] < cap[idx[j]]) {
+      ++ns[idx[j]];
+      ++n;
+    }
+  if (n * g.Hkv > 0xFFFF) return false;
+  // launch order: decreasing piece cost (LPT), then unit index
+  std::stable_sort(idx.begin(), idx.end(), [&](int p, int q) { return cost[p] / ns[p] > cost[q] / ns[q]; });
+  UnitOrder& uo = *c->chunks;
+  int pos = 0, cta = 0;
+  for (int j = 0; j < BL; ++j) {
+    const int i = idx[j];
+    for (int kvh = 0; kvh < g.Hkv; ++kvh) {
+      uo.perm[pos] = (uint16_t)(i * g.Hkv + kvh);
+      uo.pfx[pos] = (uint16_t)cta;
+      cta += ns[i];
+      ++pos;
+    }
+  }
+  uo.pfx[pos] = (uint16_t)cta;
+  uo.n_units = pos;
+  uo.n_ctas = cta;
+  return true;
+}
+
 arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, const void* q, const void* k,
                              const void* v, int32_t budget_tokens, int32_t quant_bits, void* out, int32_t out_fp32,
                              void* stream) {
@@ -1125,6 +1200,10 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
     pa.hh = &hh;
   }
   PersistPlan plan;
+  if (!persist && c->fast && build_chunks(c, layer0, n_layers, slots)) {
+    pa.chunks = c->chunks.get();
+    pa.nsplit = c->nsplit;
+  }
   if (persist) {
     build_plan(c, layer0, n_layers, 2 * c->num_sms, &plan);
     pa.plan = &plan;

@@ -59,7 +59,7 @@ __device__ __forceinline__ void combine_unit(const DecodeArgs& a, int u, int b, 
                                              float* /*sM*/, float* /*sIL*/) {
   const Geom& g = a.g;
   const int d = g.d;
-  const int S = a.n_splits;
+  const int S = a.nsplit ? a.nsplit[u] : a.n_splits;
   const float* part = a.partials + (int64_t)u * a.max_splits * G * (d + 2);
   const int64_t obase = ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * G) * d;
   // one thread per (head, dim); each merges its head's split statistics itself (redundant

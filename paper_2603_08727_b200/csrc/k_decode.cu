@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const Hh
   if ((int)threadIdx.x < G) {
     const float* part = a.partials + (int64_t)u * a.max_splits * G * (g.d + 2);
     float M, L, O;
-    merge_splits<G, false>(part, threadIdx.x, 0, a.n_splits, g.d, M, L, O);
+    merge_splits<G, false>(part, threadIdx.x, 0, a.nsplit ? a.nsplit[u] : a.n_splits, g.d, M, L, O);
     sM[threadIdx.x] = M;
     sIL[threadIdx.x] = 1.0f / L;
   }
@@ -414,7 +414,7 @@ void launch_decode_hh_acc(const DecodeArgs& a, int n_units_call, int max_rows, c
 
 // k_decode_fast.cu: returns -1 if the cache is not eligible.
 int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
-                       const PersistPlan* plan, const HhPlan* hh, int acc_rows);
+                       const PersistPlan* plan, const HhPlan* hh, int acc_rows, const UnitOrder* chunks);
 void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s);
 
 
@@ -475,6 +475,7 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
   a.logits = logits;
   a.mstat = mstat;
   a.counters = counters;
+  a.nsplit = (fast && plan.chunks && !plan.plan) ? plan.nsplit : nullptr;
   {
     a.q_group = tuning_knob("ARKV_QGROUP", 0);          // default: as many Q tiles as fit a stage
     a.interleave = tuning_knob("ARKV_INTERLEAVE", 0);   // measured: interleaving O/Q items is slower
@@ -496,7 +497,8 @@ int launch_decode(const Geom& g, int layer0, int n_layers, const uint16_t* q, co
   const int n_units_call = g.batch * n_layers * g.Hkv;
   int n = -1;
   if (fast) {
-    n = launch_decode_fast(a, n_units_call, s, ev0, ev1, plan.plan, acc_rows > 0 ? plan.hh : nullptr, acc_rows);
+    n = launch_decode_fast(a, n_units_call, s, ev0, ev1, plan.plan, acc_rows > 0 ? plan.hh : nullptr, acc_rows,
+                           a.nsplit ? plan.chunks : nullptr);
     if (n < 0) return n;
     if (n >= 100) return n - 100;  // the combine folded the HH accumulation
   } else {

@@ -678,9 +678,25 @@ __device__ __forceinline__ void acc_reduce_rows(Acc<NG>& s) {
   }
 }
 
+#ifdef ARKV_TUNING_KNOBS
+// Tuning builds only: per-CTA start/end (globaltimer), SM id and unit/split of the split-K
+// decode kernel, read back by arkv_debug_cta_times (scripts/cta_timeline.py).
+constexpr int kCtaTimesMax = 16384;
+__device__ unsigned long long g_cta_t[kCtaTimesMax][8];
+__device__ int g_cta_on;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
+  return t;
+}
+#endif
+
 template <int G, int NG, int C, int SPW, bool F8>
 __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kStageBytes) ? 2 : 1)
-    decode_fast_kernel(DecodeArgs a) {
+    decode_fast_kernel(DecodeArgs a, const __grid_constant__ UnitOrder cl) {
+#ifdef ARKV_TUNING_KNOBS
+  const unsigned long long t_start = gtimer();
+#endif
   constexpr int kConsumers = C;
   constexpr int kStages = C * SPW;
   auto stage_of = [](int i) { return (i % C) + C * ((i / C) % SPW); };
@@ -692,8 +708,23 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
 
-  // unit of this CTA
-  const int ul = blockIdx.y;
+  // unit and split of this CTA: from the cost-balanced launch list, or the uniform grid
+  int ul, s, S;
+  if (cl.n_units > 0) {
+    const int c = blockIdx.x;
+    int lo = 0, hi = cl.n_units - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if ((int)cl.pfx[mid] <= c) lo = mid; else hi = mid - 1;
+    }
+    ul = cl.perm[lo];
+    s = c - cl.pfx[lo];
+    S = cl.pfx[lo + 1] - cl.pfx[lo];
+  } else {
+    ul = blockIdx.y;
+    s = blockIdx.x;
+    S = a.n_splits;
+  }
   const int b = ul / (a.n_layers * g.Hkv);
   const int rem = ul % (a.n_layers * g.Hkv);
   const int li = rem / g.Hkv, kvh = rem % g.Hkv;
@@ -704,7 +735,7 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
   const bool accm = (t_pos >= dsc.acc0) && (t_pos < dsc.trig);
   const int tiles_o = (n_o + 1 + kTile - 1) / kTile;
   const int tiles_q = (n_q + kTile - 1) / kTile;
-  const int S = a.n_splits, s = blockIdx.x;
+  if (a.nsplit && s == 0 && threadIdx.x == 0) a.nsplit[u] = S;  // for the combine
   const int o0 = (int)((int64_t)s * tiles_o / S), o1 = (int)((int64_t)(s + 1) * tiles_o / S);
   const int q0 = (int)((int64_t)s * tiles_q / S), q1 = (int)((int64_t)(s + 1) * tiles_q / S);
   // work items: single Original tiles and groups of up to q_per Quantized tiles (the
@@ -867,10 +898,8 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
     const int src_t = G >= 2 ? ((2 * tq) % G) / 2 : 0;
     const int src_lane = (lane & ~3) | src_t;
 
-    for (int i = warp; i < n_work; i += kConsumers) {
-      const int st = stage_of(i);
-      mbar_wait(&sm.full[st], phase_of(i) & 1);
-      __syncwarp();  // lanes may leave the spin-wait in different iterations; mma/movmatrix are .aligned
+    // one work item (staged in stage st) folded into the warp's flash state
+    auto consume_item = [&](int i, int st) {
       bool isq;
       int first, ntiles;
       item_of(i, isq, first, ntiles);
@@ -884,6 +913,23 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
         consume_tile<G, NG, F8>(tb, isq, n_valid, lrow, row_stride, lpol, qf, acc, c2, sym, lane, src_lane);
       }
       __syncwarp();
+    };
+#ifdef ARKV_TUNING_KNOBS
+    auto stamp_first = [&](int i) {
+      if (i == 0 && lane == 0 && g_cta_on) {
+        const int ci = cl.n_units > 0 ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+        if (ci < kCtaTimesMax) g_cta_t[ci][4] = gtimer();
+      }
+    };
+#else
+    auto stamp_first = [](int) {};
+#endif
+    for (int i = warp; i < n_work; i += kConsumers) {
+      const int st = stage_of(i);
+      mbar_wait(&sm.full[st], phase_of(i) & 1);
+      __syncwarp();  // lanes may leave the spin-wait in different iterations; mma/movmatrix are .aligned
+      stamp_first(i);
+      consume_item(i, st);
       if (self_refill) {
         if (lane == 0 && i + kStages < n_work) {
           // this warp's reads of the stage (generic proxy) before the refill (async proxy)
@@ -895,6 +941,12 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
       }
     }
     if (self_refill && warp == 0 && lane == 0) griddep_launch_dependents();  // PDL (the combine waits for us)
+#ifdef ARKV_TUNING_KNOBS
+    if (lane == 0 && g_cta_on && warp < 3) {
+      const int ci = cl.n_units > 0 ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+      if (ci < kCtaTimesMax) g_cta_t[ci][5 + warp] = gtimer();
+    }
+#endif
     // ---- per-warp finalisation: reduce l and z over the 8 row lanes ----
     acc_reduce_rows(acc);
     if (gq == 0) {
@@ -959,6 +1011,19 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
       part[h * (D + 2) + 1] = L;
     }
   }
+#ifdef ARKV_TUNING_KNOBS
+  if (threadIdx.x == 0 && g_cta_on) {
+    const int ci = cl.n_units > 0 ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+    if (ci < kCtaTimesMax) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;\n" : "=r"(smid));
+      g_cta_t[ci][0] = t_start;
+      g_cta_t[ci][1] = gtimer();
+      g_cta_t[ci][2] = ((unsigned long long)smid << 32) | (unsigned)(u * 64 + s);
+      g_cta_t[ci][3] = ((unsigned long long)(o1 - o0) << 32) | (unsigned)(q1 - q0);
+    }
+  }
+#endif
   // ---- fused combine: the last split CTA of the unit to finish merges all partials ----
   if (!a.fuse_combine) return;
   __threadfence();
@@ -976,13 +1041,20 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
 }
 
 template <int G, int NG, int C, int SPW, bool F8 = false>
-static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                       const UnitOrder* cl) {
   const int smem = (int)sizeof(Smem<C, SPW>);
-  dim3 grid(a.n_splits, n_units_call);
+  static UnitOrder uniform = [] {
+    UnitOrder u;
+    u.n_units = 0;
+    u.n_ctas = 0;
+    return u;
+  }();
+  const dim3 grid = cl ? dim3(cl->n_ctas) : dim3(a.n_splits, n_units_call);
   auto kern = decode_fast_kernel<G, NG, C, SPW, F8>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (ev0) cudaEventRecord(ev0, s);
-  launch_pdl(kern, grid, dim3((C + 1) * 32), (size_t)smem, s, a);
+  launch_pdl(kern, grid, dim3((C + 1) * 32), (size_t)smem, s, a, cl ? *cl : uniform);
   if (ev1) cudaEventRecord(ev1, s);
 }
 
@@ -994,34 +1066,36 @@ static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
 // measurement in tuning builds (-DARKV_TUNING_KNOBS) with ARKV_FAST_CFG=10*C+SPW (41 | 42 | 62 |
 // 43 | 81 | 22 | 23); the shipped library instantiates only the default.
 template <int G, int NG>
-static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                      const UnitOrder* cl) {
   if (a.g.mode == ARKV_QUANT_FP8) {
-    launch_cfg<G, NG, 3, 2, true>(a, n_units_call, s, ev0, ev1);
+    launch_cfg<G, NG, 3, 2, true>(a, n_units_call, s, ev0, ev1, cl);
     return;
   }
 #ifdef ARKV_TUNING_KNOBS
   if (G == 4 && NG == 1) {
     switch (tuning_knob("ARKV_FAST_CFG", 32)) {
-      case 42: launch_cfg<G, NG, 4, 2>(a, n_units_call, s, ev0, ev1); return;
-      case 62: launch_cfg<G, NG, 6, 2>(a, n_units_call, s, ev0, ev1); return;
-      case 43: launch_cfg<G, NG, 4, 3>(a, n_units_call, s, ev0, ev1); return;
-      case 81: launch_cfg<G, NG, 8, 1>(a, n_units_call, s, ev0, ev1); return;
-      case 41: launch_cfg<G, NG, 4, 1>(a, n_units_call, s, ev0, ev1); return;
-      case 22: launch_cfg<G, NG, 2, 2>(a, n_units_call, s, ev0, ev1); return;
-      case 23: launch_cfg<G, NG, 2, 3>(a, n_units_call, s, ev0, ev1); return;
+      case 42: launch_cfg<G, NG, 4, 2>(a, n_units_call, s, ev0, ev1, cl); return;
+      case 62: launch_cfg<G, NG, 6, 2>(a, n_units_call, s, ev0, ev1, cl); return;
+      case 43: launch_cfg<G, NG, 4, 3>(a, n_units_call, s, ev0, ev1, cl); return;
+      case 81: launch_cfg<G, NG, 8, 1>(a, n_units_call, s, ev0, ev1, cl); return;
+      case 41: launch_cfg<G, NG, 4, 1>(a, n_units_call, s, ev0, ev1, cl); return;
+      case 22: launch_cfg<G, NG, 2, 2>(a, n_units_call, s, ev0, ev1, cl); return;
+      case 23: launch_cfg<G, NG, 2, 3>(a, n_units_call, s, ev0, ev1, cl); return;
       default: break;
     }
   }
 #endif
-  launch_cfg<G, NG, 3, 2>(a, n_units_call, s, ev0, ev1);
+  launch_cfg<G, NG, 3, 2>(a, n_units_call, s, ev0, ev1, cl);
 }
 
 template <int G>
-static int launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1) {
+static int launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                    const UnitOrder* cl) {
   switch (a.g.ng) {
-    case 1: launch_gn<G, 1>(a, n_units_call, s, ev0, ev1); return 0;
-    case 2: launch_gn<G, 2>(a, n_units_call, s, ev0, ev1); return 0;
-    case 4: launch_gn<G, 4>(a, n_units_call, s, ev0, ev1); return 0;
+    case 1: launch_gn<G, 1>(a, n_units_call, s, ev0, ev1, cl); return 0;
+    case 2: launch_gn<G, 2>(a, n_units_call, s, ev0, ev1, cl); return 0;
+    case 4: launch_gn<G, 4>(a, n_units_call, s, ev0, ev1, cl); return 0;
     default: return -1;
   }
 }
@@ -1461,7 +1535,7 @@ float decode_fast_pscale(const Geom& g) {
 }
 
 int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
-                       const PersistPlan* plan, const HhPlan* hh, int acc_rows) {
+                       const PersistPlan* plan, const HhPlan* hh, int acc_rows, const UnitOrder* chunks) {
   if (!decode_fast_available(a.g)) return -1;
   if (plan) {  // persistent range-partitioned kernel + its combine
     switch (a.g.G) {
@@ -1474,10 +1548,10 @@ int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
   }
   int r = -1;
   switch (a.g.G) {
-    case 1: r = fast::launch_g<1>(a, n_units_call, s, ev0, ev1); break;
-    case 2: r = fast::launch_g<2>(a, n_units_call, s, ev0, ev1); break;
-    case 4: r = fast::launch_g<4>(a, n_units_call, s, ev0, ev1); break;
-    case 8: r = fast::launch_g<8>(a, n_units_call, s, ev0, ev1); break;
+    case 1: r = fast::launch_g<1>(a, n_units_call, s, ev0, ev1, chunks); break;
+    case 2: r = fast::launch_g<2>(a, n_units_call, s, ev0, ev1, chunks); break;
+    case 4: r = fast::launch_g<4>(a, n_units_call, s, ev0, ev1, chunks); break;
+    case 8: r = fast::launch_g<8>(a, n_units_call, s, ev0, ev1, chunks); break;
     default: return -1;
   }
   if (r < 0) return -1;
@@ -1491,3 +1565,17 @@ int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
 }
 
 }  // namespace arkv
+
+#ifdef ARKV_TUNING_KNOBS
+// on >= 0: enable/disable recording; out != nullptr: copy n records (8 x u64 each: start, end,
+// smid << 32 | unit * 64 + split, O tiles << 32 | Q tiles, first item staged, warp 0..2 done).
+extern "C" int arkv_debug_cta_times(int on, unsigned long long* out, int n) {
+  if (on >= 0) cudaMemcpyToSymbol(arkv::fast::g_cta_on, &on, sizeof(int));
+  if (out) {
+    cudaDeviceSynchronize();
+    n = n < arkv::fast::kCtaTimesMax ? n : arkv::fast::kCtaTimesMax;
+    cudaMemcpyFromSymbol(out, arkv::fast::g_cta_t, (size_t)n * 8 * sizeof(unsigned long long));
+  }
+  return (int)cudaGetLastError();
+}
+#endif

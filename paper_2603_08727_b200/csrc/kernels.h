@@ -93,6 +93,8 @@ struct DecodeArgs {
   float* logits;
   float* mstat;  // [unit][G][2]: merged max (log2) and 1/sum of the step, for the HH kernel
   int32_t* counters;  // [unit]: split CTAs finished this step (fused combine); reset by the last
+  int32_t* nsplit;    // [unit]: this step's split count, written by split 0 of the chunk-list
+                      // launch (UnitOrder) and read by the combines; nullptr: every unit n_splits
   int q_group;        // fast kernel: Quantized tiles per bulk copy (0 = as many as fit a stage)
   int interleave;     // fast kernel: interleave Original and Quantized work items
   int fuse_combine;   // fast kernel: the last split CTA of a unit merges the partials
@@ -152,7 +154,24 @@ struct HhPlan {
                           // z = 1 on the window's first step (acc := sample); w = n_q
   int coff[kMaxHhEntries + 1];  // first chunk of each entry (its own row count: no empty blocks)
 };
+// Split-K launch order of the fast decode kernel ("cost-balanced splits").
+// The host gives each unit a split count in proportion to its estimated time (Original tiles
+// + Quantized tiles weighted by their measured relative cost; in all exactly `waves` CTAs per
+// CTA slot) and orders the units by piece cost, longest first (LPT), so the last wave is
+// filled by the shortest pieces.  CTA c of the 1-D grid runs split c - pfx[i] of unit perm[i]
+// for the i with pfx[i] <= c < pfx[i + 1].  Passed by value as a kernel parameter (kept
+// small: a 16 KB per-CTA list measured +7 us of launch latency per step).  n_units = 0: the
+// uniform grid (n_splits x units).
+constexpr int kMaxOrderUnits = 1024;
+struct UnitOrder {
+  int n_units;
+  int n_ctas;
+  uint16_t perm[kMaxOrderUnits];     // unit (index in the call) of each position
+  uint16_t pfx[kMaxOrderUnits + 1];  // first CTA of each position
+};
 struct PlanArgs {
+  const UnitOrder* chunks = nullptr;  // split-K fast kernel: cost-balanced launch order, or nullptr
+  int32_t* nsplit = nullptr;          // [unit] split counts of a chunk-list launch (workspace)
   const HhPlan* hh = nullptr;         // fused HH plan (split-K fast kernel), or nullptr
   const PersistPlan* plan = nullptr;  // host plan, or nullptr: split-K kernels
   float* pparts = nullptr;
