@@ -1189,10 +1189,12 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   }
   PlanArgs pa;
   static const bool fuse_hh = tuning_knob("ARKV_FUSE_HH", 1) != 0;
-  // auto kernel choice per call: the persistent range-partitioned kernel also when most of
-  // the call's bytes are Quantized tiles (ALU-heavy items: its equal per-CTA ranges beat
-  // split-K's per-unit splits; measured in Base_quant mode: 0.68 vs 0.51 of the copy peak)
-  static const int q_share_pct = tuning_knob("ARKV_PERSIST_QSHARE", 60);
+  // auto kernel choice per call: round 2's rule also took the persistent range-partitioned
+  // kernel when >= 60 % of a call's bytes were Quantized tiles (then 0.68 vs 0.51 of the copy
+  // peak).  The chunked split-K pipeline with cost-balanced splits beats it there too (rho = 0
+  // at configs[1], HH window: kernel 0.218 vs 0.221 ms, step 0.238 vs 0.249 ms), so the
+  // Quantized-share switch is off (ARKV_PERSIST_QSHARE, tuning builds, restores it).
+  static const int q_share_pct = tuning_knob("ARKV_PERSIST_QSHARE", 101);
   const bool persist = c->persist || (c->fast && c->cfg.decode_kernel == 0 &&
                                       seg_q > 0.01 * q_share_pct * (seg_o + seg_q));
   if (acc_rows > 0 && hh_fit && fuse_hh && !persist) {

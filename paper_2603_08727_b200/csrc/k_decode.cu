@@ -294,8 +294,10 @@ static int combine_threads(const Geom& g) { return std::min(1024, std::max(128, 
 // decode_hh_acc launch and its drain).  Combine blocks as decode_combine; an HH block
 // recomputes its unit's merged (M, 1/L) with the combine's own code (bit-identical), then
 // folds rows [chunk * R, chunk * R + R) exactly as decode_hh_acc does.
+// (8 rows per thread run as 256-thread blocks: bounding them at 256 threads leaves the rows'
+// logits and accumulators in registers — at 1024 the 64-register cap spilled them)
 template <int G, int kHhRowsPerThread>
-__global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const HhPlan hp) {
+__global__ void __launch_bounds__(kHhRowsPerThread == 8 ? 256 : 1024) decode_combine_hh(DecodeArgs a, const HhPlan hp) {
   griddep_wait();
   griddep_launch_dependents();
   const Geom& g = a.g;
@@ -346,18 +348,36 @@ __global__ void __launch_bounds__(1024) decode_combine_hh(DecodeArgs a, const Hh
 #pragma unroll
       for (int h = 0; h < G; ++h) lg[k][h] = ok ? ld_hint(lp + h, pol) : 0.f;
     }
+  }
+  // the accumulators' addresses wait for the descriptor's slot: loaded after every logit load
+  // has been issued
+#pragma unroll
+  for (int k = 0; k < kHhRowsPerThread; ++k) {
+    const int i = r0 + threadIdx.x + k * blockDim.x;
     ac[k] = make_float2(0.f, 0.f);
-    if (ok && !first) ac[k] = ld_hint(isq ? &sm.acc_q[i - n_o] : &sm.acc_o[i], pol);
+    if (i < n_rows && !first) ac[k] = ld_hint(i >= n_o ? &sm.acc_q[i - n_o] : &sm.acc_o[i], pol);
   }
-  __shared__ float sM[G], sIL[G];
-  if ((int)threadIdx.x < G) {
-    const float* part = a.partials + (int64_t)u * a.max_splits * G * (g.d + 2);
-    float M, L, O;
-    merge_splits<G, false>(part, threadIdx.x, 0, a.nsplit ? a.nsplit[u] : a.n_splits, g.d, M, L, O);
-    sM[threadIdx.x] = M;
-    sIL[threadIdx.x] = 1.0f / L;
+  // the unit's merged (M, 1/L) per head, merged by each warp itself (lane h merges head h
+  // with the combine's code, bit for bit, and broadcasts it): no block barrier between the
+  // rows' loads and their use (a __syncthreads here was the kernel's top stall)
+  float sM[G], sIL[G];
+  {
+    const int lane = threadIdx.x & 31;
+    float mh = 0.f, ilh = 0.f;
+    if (lane < G) {
+      const float* part = a.partials + (int64_t)u * a.max_splits * G * (g.d + 2);
+      float M, L, O;
+      merge_splits<G, false>(part, lane, 0, a.nsplit ? a.nsplit[u] : a.n_splits, g.d, M, L, O);
+      mh = M;
+      ilh = 1.0f / L;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      sM[h] = __shfl_sync(0xffffffffu, mh, h);
+      sIL[h] = __shfl_sync(0xffffffffu, ilh, h);
+    }
   }
-  __syncthreads();
 #pragma unroll
   for (int k = 0; k < kHhRowsPerThread; ++k) {
     const int i = r0 + threadIdx.x + k * blockDim.x;

@@ -366,18 +366,20 @@ __device__ __forceinline__ void acc_reset(Acc<NG>& s) {
   }
 }
 
-// Folds one staged 32-token tile into the warp's flash state.  tb: the tile in shared
-// memory; n_valid: rows in use; lrow: HH logits of this tile's first row, [row][G] (a.logits
-// + (u row_stride + (isq ? cap_o : 0) + 32 tile) G) or nullptr outside the HH window.
+// Tile processing, in three parts so a pipeline may stage an Original tile's K block and
+// V^T block separately: qk_softmax (S = K q^T, HH logits, online-softmax update -> p),
+// then pv_orig (Original tiles: O^T += V^T P'^T on the V^T block) or pv_quant (Quantized
+// tiles, same staged tile).  consume_tile = the three for a tile staged whole.
+// tb: the tile (or its K block) in shared memory; n_valid: rows in use; lrow: HH logits of
+// this tile's first row, [row][G] (a.logits + (u row_stride + (isq ? cap_o : 0) + 32 tile) G)
+// or nullptr outside the HH window.
 template <int G, int NG, bool F8>
-__device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_valid, float* lrow, int row_stride,
-                                             uint64_t lpol,
-                                             const QFrag<NG>& f, Acc<NG>& s, float c2, bool sym, int lane,
-                                             int src_lane) {
+__device__ __forceinline__ void qk_softmax(const uint8_t* tb, bool isq, int n_valid, float* lrow, uint64_t lpol,
+                                           const QFrag<NG>& f, Acc<NG>& s, float c2, bool sym, int lane,
+                                           int src_lane, float (&p)[2][4], float (&zv)[2][2][NG]) {
   const int gq = lane >> 2, tq = lane & 3;
   // ---- S = K q^T, logits in the log2 domain ----
-  float lg[2][4];      // [m-tile][(row g|g+8) x (col 2t|2t+1)]
-  float zv[2][2][NG];  // Quantized: z_v of rows (g, g+8) per m-tile, per group
+  float lg[2][4];  // [m-tile][(row g|g+8) x (col 2t|2t+1)]; zv: Quantized z_v of rows (g, g+8)
   if (!isq) {
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
@@ -545,7 +547,6 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
       s.o[mv][3] *= c1;
     }
   }
-  float p[2][4];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -554,20 +555,25 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
       p[mt][e] = (mm == -INFINITY) ? 0.f : ex2_ftz(lg[mt][e] - (mm + kPScale<F8>));  // ex2(-inf) = 0 for masked rows
       s.l_run[e & 1] += p[mt][e];
     }
+}
 
-  if (!isq) {
-    // ---- PV on Original tiles (bf16) ----
+// PV of an Original tile; vb: its V^T block in shared memory
+template <int G, int NG>
+__device__ __forceinline__ void pv_orig(const uint8_t* vb, int n_valid, const float (&p)[2][4], Acc<NG>& s,
+                                        int lane) {
+  const int tq = lane & 3;
+  {
     if (n_valid < kTile) {
       // rows past the segment may hold stale bytes (NaN patterns): P' = 0 there, but
       // 0 * NaN = NaN inside the MMA, so zero them in the staged copy
-      uint8_t* tw = const_cast<uint8_t*>(tb);
+      uint8_t* tw = const_cast<uint8_t*>(vb);
       for (int idx = lane; idx < (kTile - n_valid) * D; idx += 32) {
         const int j = n_valid + idx / D, x = idx % D;
         // FRAG V offset (common.cuh o_v_off) for d = 128
         const int mtv = x >> 4, r = x & 15, gg = r & 7, sel = r >> 3;
         const int kc = j >> 4, jj = j & 15, hi = jj >> 3, tt = jj & 7, t = tt >> 1, uu = tt & 1;
         const int k = (mtv * 2 + kc) * 4 + sel + 2 * hi;
-        *(uint16_t*)(tw + 64 * D + lane_word(k, 4 * gg + t) * 4 + uu * 2) = 0;
+        *(uint16_t*)(tw + lane_word(k, 4 * gg + t) * 4 + uu * 2) = 0;
       }
       // order these generic-proxy writes before the stage's next TMA (async-proxy) fill
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -576,7 +582,6 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
     uint32_t b01[2], b23[2], c01[2], c23[2];
 #pragma unroll
     for (int kc = 0; kc < 2; ++kc) make_b<G, true>(p[kc], tq, b01[kc], b23[kc], c01[kc], c23[kc]);
-    const uint8_t* vb = tb + 64 * D;
 #pragma unroll
     for (int mv = 0; mv < 8; ++mv) {
 #pragma unroll
@@ -586,7 +591,15 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
         if (G == 8) mma_bf16(s.o[mv], r.x, r.y, r.z, r.w, c01[kc], c23[kc]);
       }
     }
-  } else if (F8) {
+  }
+}
+
+// PV of a Quantized tile staged whole (tb)
+template <int G, int NG, bool F8>
+__device__ __forceinline__ void pv_quant(const uint8_t* tb, const float (&p)[2][4], const float (&zv)[2][2][NG],
+                                         Acc<NG>& s, int lane) {
+  const int gq = lane >> 2, tq = lane & 3;
+  if (F8) {
     // ---- PV on fp8 Quantized tiles: A = e4m3 V^T (converted), B = P' = p·s_v ----
     const float* sc = (const float*)(tb + 64 * D);
     uint32_t b01[NG][2], b23[NG][2], c01[NG][2], c23[NG][2];
@@ -662,6 +675,19 @@ __device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_
       }
     }
   }
+}
+
+template <int G, int NG, bool F8>
+__device__ __forceinline__ void consume_tile(const uint8_t* tb, bool isq, int n_valid, float* lrow, int /*row_stride*/,
+                                             uint64_t lpol, const QFrag<NG>& f, Acc<NG>& s, float c2, bool sym,
+                                             int lane, int src_lane) {
+  float p[2][4];
+  float zv[2][2][NG];
+  qk_softmax<G, NG, F8>(tb, isq, n_valid, lrow, lpol, f, s, c2, sym, lane, src_lane, p, zv);
+  if (!isq)
+    pv_orig<G, NG>(tb + 64 * D, n_valid, p, s, lane);
+  else
+    pv_quant<G, NG, F8>(tb, p, zv, s, lane);
 }
 
 // Reduces l and z over the 8 row lanes (every lane ends with its heads' sums).
@@ -1040,6 +1066,341 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// "Chunked" split-K pipeline (default): 3 CTAs per SM of 3 consumer warps each
+// and no producer warp — every warp streams its own chunks through 2 private 12 KB stages
+// (self-refill).  An Original tile is two chunks (its 8 KB K block, then its 8 KB V^T block);
+// Quantized tiles go two per chunk (9 KB).  9 consumer warps per SM instead of 6: the
+// Quantized path is issue-bound (fixed-latency dependency stalls with 1.5 warps per
+// scheduler), the Original path HBM-bound either way.  The step's token (D1) is appended
+// by warp 0 before it waits for its first chunk.
+// ---------------------------------------------------------------------------------------
+constexpr int kChunkBytes = 12288;
+template <int C>
+struct Smem3 {
+  static constexpr int kStages = 2 * C;
+  uint8_t ring[kStages][kChunkBytes];
+  uint64_t full[kStages];
+  float wm[C][8];
+  float wl[C][8];
+  float wz[C][8][4];
+  float newtok[8];
+};
+
+template <int G, int NG, bool F8, int C>
+__global__ void __launch_bounds__(C * 32, C == 3 ? 3 : 2) decode_chunk_kernel(DecodeArgs a,
+                                                                              const __grid_constant__ UnitOrder cl) {
+#ifdef ARKV_TUNING_KNOBS
+  const unsigned long long t_start = gtimer();
+#endif
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem3<C>& sm = *reinterpret_cast<Smem3<C>*>(smem_raw);
+  const Geom& g = a.g;
+  griddep_wait();  // PDL: the previous kernel (tailor / combine) has completed
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  int ul, s, S;
+  if (cl.n_units > 0) {
+    const int c = blockIdx.x;
+    int lo = 0, hi = cl.n_units - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if ((int)cl.pfx[mid] <= c) lo = mid; else hi = mid - 1;
+    }
+    ul = cl.perm[lo];
+    s = c - cl.pfx[lo];
+    S = cl.pfx[lo + 1] - cl.pfx[lo];
+  } else {
+    ul = blockIdx.y;
+    s = blockIdx.x;
+    S = a.n_splits;
+  }
+  const int b = ul / (a.n_layers * g.Hkv);
+  const int rem = ul % (a.n_layers * g.Hkv);
+  const int li = rem / g.Hkv, kvh = rem % g.Hkv;
+  const int u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
+  const UnitDesc dsc = a.desc[u];
+  uint8_t* slot = a.slots + (int64_t)dsc.slot * g.slot_bytes;
+  const int n_o = dsc.n_o, n_q = dsc.n_q, t_pos = dsc.t_next;
+  const bool accm = (t_pos >= dsc.acc0) && (t_pos < dsc.trig);
+  const int tiles_o = (n_o + 1 + kTile - 1) / kTile;
+  const int tiles_q = (n_q + kTile - 1) / kTile;
+  if (a.nsplit && s == 0 && threadIdx.x == 0) a.nsplit[u] = S;  // for the combine
+  const int o0 = (int)((int64_t)s * tiles_o / S), o1 = (int)((int64_t)(s + 1) * tiles_o / S);
+  const int q0 = (int)((int64_t)s * tiles_q / S), q1 = (int)((int64_t)(s + 1) * tiles_q / S);
+  const int q_per = max(1, kChunkBytes / g.tile_q);  // Quantized tiles per chunk (int4: 2 x 4.5 KB; fp8: 1)
+  const int n_oi = o1 - o0, n_qi = (q1 - q0 + q_per - 1) / q_per;
+  const int n_work = n_oi + n_qi;
+  const bool rev = a.item_order == 2 || (a.item_order == 1 && ((s + ul) & 1));
+  // item i -> Original tile (1 item = 2 chunks) or a group of <= 2 Quantized tiles (1 chunk)
+  auto item_of = [&](int i, bool& isq, int& first, int& ntiles) {
+    if (rev) i = i < n_qi ? n_oi + i : i - n_qi;  // Quantized groups first
+    isq = i >= n_oi;
+    if (!isq) {
+      first = o0 + i;
+      ntiles = 1;
+    } else {
+      first = q0 + (i - n_oi) * q_per;
+      ntiles = min(q_per, q1 - first);
+    }
+  };
+  const bool owns_new = (o0 <= n_o / kTile) && (n_o / kTile < o1);
+  const int row_stride = g.cap_o + g.cap_q;
+  const int64_t qkv = (int64_t)(b * a.n_layers + li);
+  const uint16_t* qp = a.q + (qkv * g.Hq + kvh * G) * D;
+  const uint16_t* kn = a.k + (qkv * g.Hkv + kvh) * D;
+  const uint16_t* vn = a.v + (qkv * g.Hkv + kvh) * D;
+  const float c2 = g.sm_scale * kLog2e;
+  const bool sym = g.mode == ARKV_QUANT_SYM;
+  // stage barriers: each warp initialises its own two (nobody else touches them)
+  if (lane == 0) {
+    mbar_init(&sm.full[2 * warp], 1);
+    mbar_init(&sm.full[2 * warp + 1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t lpol = l2_evict_last();  // HH logits stay in L2 for the combine
+  const uint64_t pol_stream = l2_evict_first();
+  // the warp's chunk cursor: (item, part); part 1 = the V^T block of an Original tile
+  struct Cur {
+    int i, part;
+  };
+  auto chunk_src = [&](const Cur& c, const uint8_t*& src, uint32_t& bytes) {
+    bool isq;
+    int first, ntiles;
+    item_of(c.i, isq, first, ntiles);
+    if (isq) {
+      src = q_tile_ptr(slot, g, first + ntiles - 1);
+      bytes = (uint32_t)(ntiles * g.tile_q);
+    } else {
+      src = o_tile_ptr(slot, g, first) + (c.part ? 64 * D : 0);
+      bytes = (uint32_t)(32 * D * 2);
+    }
+  };
+  auto next = [&](Cur c) {
+    bool isq;
+    int first, ntiles;
+    item_of(c.i, isq, first, ntiles);
+    if (!isq && c.part == 0) return Cur{c.i, 1};
+    return Cur{c.i + C, 0};
+  };
+  auto issue = [&](const Cur& c, int st) {  // lane 0
+    const uint8_t* src;
+    uint32_t bytes;
+    chunk_src(c, src, bytes);
+    mbar_expect_tx(&sm.full[st], bytes);
+    if (a.l2_hints)
+      bulk_g2s_hint(sm.ring[st], src, bytes, &sm.full[st], pol_stream);
+    else
+      bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
+  };
+  Cur fetch{warp, 0};
+  if (lane == 0) {
+    for (int k = 0; k < 2 && fetch.i < n_work; ++k) {
+      issue(fetch, 2 * warp + k);
+      fetch = next(fetch);
+    }
+  }
+  fetch = Cur{warp, 0};
+  fetch = next(next(fetch));  // every lane tracks the cursor (lane 0 issued the first two)
+  if (warp == 0 && owns_new) {
+    // the step's token (D1): appended while the first chunks are in flight
+    if (warp_step_nonfinite(qp, G * D, kn, vn, D, lane) && lane == 0) atomicOr(a.err, kErrNonFinite);
+    const int tt = n_o / kTile, j = n_o % kTile;
+    const SlotMeta meta = slot_meta(a.meta, g, dsc.slot);
+    const bool fits = (n_o + 1 <= g.cap_o) &&
+                      ((int64_t)tiles_o * g.tile_o + (int64_t)tiles_q * g.tile_q <= g.slot_bytes);
+    if (!fits) {
+      if (lane == 0) atomicOr(a.err, kErrCapacity);
+    } else {
+      uint8_t* tb = o_tile_ptr(slot, g, tt);
+      for (int x = lane; x < D; x += 32) {
+        *(uint16_t*)(tb + o_k_off(g, j, x)) = kn[x];
+        *(uint16_t*)(tb + o_v_off(g, j, x)) = vn[x];
+      }
+      if (lane == 0) {
+        meta.pos_o[n_o] = t_pos;
+        meta.acc_o[n_o] = make_float2(0.f, 0.f);
+      }
+    }
+    float kx[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) kx[i] = bf16_to_f(kn[lane * 4 + i]);
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc = fmaf(bf16_to_f(qp[h * D + lane * 4 + i]), kx[i], acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) sm.newtok[h] = acc * c2;
+    }
+    __syncwarp();
+    if (accm && lane < G)
+      st_hint(a.logits + ((int64_t)u * row_stride + n_o) * G + lane, sm.newtok[lane], l2_evict_last());
+  }
+  QFrag<NG> qf;
+  load_qfrag<G, NG, F8>(qp, lane, qf);
+  Acc<NG> acc;
+  acc_reset(acc);
+  const int src_t = G >= 2 ? ((2 * tq) % G) / 2 : 0;
+  const int src_lane = (lane & ~3) | src_t;
+  float p[2][4];        // an Original tile's probabilities, from its K chunk to its V chunk
+  int o_valid = kTile;  // ... and its rows in use
+  Cur cur{warp, 0};
+  uint32_t ph = 0;
+  int k = 0;
+#ifdef ARKV_TUNING_KNOBS
+  bool first_chunk = true;
+#endif
+  while (cur.i < n_work) {
+    const int st = 2 * warp + k;
+    mbar_wait(&sm.full[st], (ph >> k) & 1u);
+    __syncwarp();
+#ifdef ARKV_TUNING_KNOBS
+    if (first_chunk && warp == 0 && lane == 0 && g_cta_on) {
+      const int ci = cl.n_units > 0 ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+      if (ci < kCtaTimesMax) g_cta_t[ci][4] = gtimer();
+    }
+    first_chunk = false;
+#endif
+    bool isq;
+    int first, ntiles;
+    item_of(cur.i, isq, first, ntiles);
+    const uint8_t* tb = sm.ring[st];
+    if (isq) {
+      for (int jt = 0; jt < ntiles; ++jt) {
+        const int tile = first + jt;
+        const int n_valid = min(kTile, n_q - tile * kTile);
+        float* lrow = accm ? a.logits + ((int64_t)u * row_stride + g.cap_o + tile * kTile) * G : nullptr;
+        float pq[2][4];
+        float zv[2][2][NG];
+        const uint8_t* tq_ = tb + (ntiles - 1 - jt) * g.tile_q;
+        qk_softmax<G, NG, F8>(tq_, true, n_valid, lrow, lpol, qf, acc, c2, sym, lane, src_lane, pq, zv);
+        pv_quant<G, NG, F8>(tq_, pq, zv, acc, lane);
+      }
+    } else if (cur.part == 0) {
+      o_valid = min(kTile, n_o - first * kTile);
+      float* lrow = accm ? a.logits + ((int64_t)u * row_stride + first * kTile) * G : nullptr;
+      float zv[2][2][NG];
+      qk_softmax<G, NG, F8>(tb, false, o_valid, lrow, lpol, qf, acc, c2, sym, lane, src_lane, p, zv);
+    } else {
+      pv_orig<G, NG>(tb, o_valid, p, acc, lane);
+    }
+    __syncwarp();
+    if (lane == 0 && fetch.i < n_work) {
+      // this warp's reads of the stage (generic proxy) before the refill (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(fetch, st);
+    }
+    if (fetch.i < n_work) fetch = next(fetch);
+    cur = next(cur);
+    ph ^= 1u << k;
+    k ^= 1;
+  }
+  if (warp == 0 && lane == 0) griddep_launch_dependents();  // PDL (the combine waits for us)
+#ifdef ARKV_TUNING_KNOBS
+  if (lane == 0 && g_cta_on) {
+    const int ci = cl.n_units > 0 ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+    if (ci < kCtaTimesMax) g_cta_t[ci][5 + warp] = gtimer();
+  }
+#endif
+  acc_reduce_rows(acc);
+  if (gq == 0) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int h = 2 * tq + e;
+      if (h < G) {
+        sm.wm[warp][h] = acc.m_run[e];
+        sm.wl[warp][h] = acc.l_run[e];
+#pragma unroll
+        for (int gr = 0; gr < NG; ++gr) sm.wz[warp][h][gr] = acc.z_run[e][gr];
+      }
+    }
+  }
+  __syncthreads();  // every warp is done with the ring: reuse it for the O^T accumulators
+  {
+    float* ob = (float*)sm.ring[0] + warp * 8 * D;  // [col][dim]
+#pragma unroll
+    for (int mv = 0; mv < 8; ++mv) {
+      const int x0 = mv * 16 + gq;
+      ob[(2 * tq + 0) * D + x0] = acc.o[mv][0];
+      ob[(2 * tq + 1) * D + x0] = acc.o[mv][1];
+      ob[(2 * tq + 0) * D + x0 + 8] = acc.o[mv][2];
+      ob[(2 * tq + 1) * D + x0 + 8] = acc.o[mv][3];
+    }
+  }
+  __syncthreads();
+  // ---- CTA merge of the warps (+ the appended token) -> split partial ----
+  const float* ob = (const float*)sm.ring[0];
+  float* part = a.partials + ((int64_t)u * a.max_splits + s) * G * (D + 2);
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int h = idx / D, x = idx % D;
+    const int gr = x / (D / NG);
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < C; ++w) M = fmaxf(M, sm.wm[w][h]);
+    float snew = -INFINITY;
+    if (owns_new) {
+      snew = sm.newtok[h];
+      M = fmaxf(M, snew);
+    }
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < C; ++w) {
+      const float mw = sm.wm[w][h];
+      if (mw == -INFINITY) continue;
+      const float cw = exp2f(mw - M);
+      float ow = ob[(w * 8 + h) * D + x];
+      if (G < 8) ow += ob[(w * 8 + h + G) * D + x];
+      ow += sm.wz[w][h][gr];
+      L += sm.wl[w][h] * cw;
+      O += ow * cw;
+    }
+    if (owns_new) {
+      const float cn = exp2f(snew - M - kPScale<F8>);  // the partials' probability scale (kPvSub)
+      L += cn;
+      O += cn * bf16_to_f(vn[x]);
+    }
+    part[h * (D + 2) + 2 + x] = O;
+    if (x == 0) {
+      part[h * (D + 2) + 0] = M;
+      part[h * (D + 2) + 1] = L;
+    }
+  }
+#ifdef ARKV_TUNING_KNOBS
+  if (threadIdx.x == 0 && g_cta_on) {
+    const int ci = cl.n_units > 0 ? (int)blockIdx.x : (int)(blockIdx.y * gridDim.x + blockIdx.x);
+    if (ci < kCtaTimesMax) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;\n" : "=r"(smid));
+      g_cta_t[ci][0] = t_start;
+      g_cta_t[ci][1] = gtimer();
+      g_cta_t[ci][2] = ((unsigned long long)smid << 32) | (unsigned)(u * 64 + s);
+      g_cta_t[ci][3] = ((unsigned long long)(o1 - o0) << 32) | (unsigned)(q1 - q0);
+    }
+  }
+#endif
+}
+
+template <int G, int NG, bool F8, int C>
+static void launch_chunk(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                         const UnitOrder* cl) {
+  const int smem = (int)sizeof(Smem3<C>);
+  static UnitOrder uniform = [] {
+    UnitOrder u;
+    u.n_units = 0;
+    u.n_ctas = 0;
+    return u;
+  }();
+  const dim3 grid = cl ? dim3(cl->n_ctas) : dim3(a.n_splits, n_units_call);
+  auto kern = decode_chunk_kernel<G, NG, F8, C>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (ev0) cudaEventRecord(ev0, s);
+  launch_pdl(kern, grid, dim3(C * 32), (size_t)smem, s, a, cl ? *cl : uniform);
+  if (ev1) cudaEventRecord(ev1, s);
+}
+
 template <int G, int NG, int C, int SPW, bool F8 = false>
 static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
                        const UnitOrder* cl) {
@@ -1068,6 +1429,18 @@ static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
 template <int G, int NG>
 static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
                       const UnitOrder* cl) {
+  // 3: chunked, 3 warps x 3 CTAs/SM; 4: chunked, 4 warps x 2 CTAs/SM; 2: producer ring
+  static const int pipe = tuning_knob("ARKV_FAST_PIPE", 4);
+  if (pipe == 3 || pipe == 4) {
+    const bool f8 = a.g.mode == ARKV_QUANT_FP8;
+    if (pipe == 3)
+      f8 ? launch_chunk<G, NG, true, 3>(a, n_units_call, s, ev0, ev1, cl)
+         : launch_chunk<G, NG, false, 3>(a, n_units_call, s, ev0, ev1, cl);
+    else
+      f8 ? launch_chunk<G, NG, true, 4>(a, n_units_call, s, ev0, ev1, cl)
+         : launch_chunk<G, NG, false, 4>(a, n_units_call, s, ev0, ev1, cl);
+    return;
+  }
   if (a.g.mode == ARKV_QUANT_FP8) {
     launch_cfg<G, NG, 3, 2, true>(a, n_units_call, s, ev0, ev1, cl);
     return;

@@ -1,0 +1,9 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+python -m paper_2603_08727_b200.build > /dev/null 2>&1
+O=gpurun_out/r3_hh2; mkdir -p $O
+timeout 900 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; tail -2 $O/gpu_tests.log
+for i in 1 2; do timeout 600 python scripts/step_profile.py --steps 70 > $O/sp$i.txt 2>&1; tail -2 $O/sp$i.txt; done
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:decode_combine_hh --launch-skip 8 --launch-count 1 -o $O/combine_hh -f python scripts/step_profile.py --steps 12 > $O/ncu1.log 2>&1; tail -1 $O/ncu1.log
+timeout 600 python bench.py --steps 20 --warmup 5 > $O/bench20.json 2> $O/bench20.err; python -c "
+import json;d=json.loads(open('$O/bench20.json').read().strip().splitlines()[-1]);print('bench20',d['value'],d['ms_per_step'],d['roofline']['frac'],d['roofline']['kernel_ms_per_launch'],d['e2e']['value'])"

@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="llama3-8b-32k")
     ap.add_argument("--steps", type=int, default=120)
+    ap.add_argument("--rho", type=float, default=None, help="override every layer's rho (0: Base_quant-like)")
     args = ap.parse_args()
     wl = bench.WORKLOADS[args.workload]
     B, L, Hq, Hkv, d, P = (wl["batch"], wl["n_layers"], wl["n_q_heads"], wl["n_kv_heads"], wl["head_dim"],
@@ -33,7 +34,8 @@ def main():
     cache = A.ArkvCache(cfg, dev)
     sh = Shape(batch=B, n_layers=L, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, prompt_len=P, window=wl["window"])
     qw, k, v = prefill_inputs_fast(sh, seed=1234, device=dev)
-    _, _, rho = cache.arkv_prefill_stats(qw, k, v)
+    ov = None if args.rho is None else [[args.rho] * L for _ in range(B)]
+    _, _, rho = cache.arkv_prefill_stats(qw, k, v, rho_override=ov)
     del qw, k, v
     pool = [decode_inputs_fast(sh, s, seed=1234, device=dev) for s in range(args.steps)]
     out = torch.empty(B, L, Hq, d, dtype=torch.bfloat16, device=dev)
