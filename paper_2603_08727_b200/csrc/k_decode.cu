@@ -408,8 +408,12 @@ void launch_decode_combine_hh(const DecodeArgs& a, const HhPlan& hp, int max_row
   const dim3 grid(p.n_units + p.n_chunks * a.g.Hkv);
 #define HH_CASE(GV)                                                                                          \
   case GV:                                                                                                   \
-    if (rpt == 8) launch_pdl(decode_combine_hh<GV, 8>, grid, dim3(threads), 0, s, a, p);                     \
-    else launch_pdl(decode_combine_hh<GV, 4>, grid, dim3(threads), 0, s, a, p);                              \
+    if (rpt == 8) {                                                                                          \
+      static const bool once = (carveout_max(decode_combine_hh<GV, 8>), true);                               \
+      (void)once;                                                                                            \
+      launch_pdl(decode_combine_hh<GV, 8>, grid, dim3(threads), 0, s, a, p);                                 \
+    } else                                                                                                   \
+      launch_pdl(decode_combine_hh<GV, 4>, grid, dim3(threads), 0, s, a, p);                                 \
     break;
   switch (a.g.G) {
     HH_CASE(1)
@@ -462,6 +466,9 @@ static void launch_g(const DecodeArgs& a, int n_units_call, cudaStream_t s, cuda
 }
 
 void launch_decode_combine(const DecodeArgs& a, int n_units_call, cudaStream_t s) {
+  static const bool once = (carveout_max(decode_combine<1>), carveout_max(decode_combine<2>),
+                            carveout_max(decode_combine<4>), carveout_max(decode_combine<8>), true);
+  (void)once;
   switch (a.g.G) {
     case 1: launch_pdl(decode_combine<1>, dim3(n_units_call), dim3(combine_threads(a.g)), 0, s, a); break;
     case 2: launch_pdl(decode_combine<2>, dim3(n_units_call), dim3(combine_threads(a.g)), 0, s, a); break;

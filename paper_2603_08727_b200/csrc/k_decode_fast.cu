@@ -1075,10 +1075,16 @@ __global__ void __launch_bounds__((C + 1) * 32, (C * SPW * kStageBytes <= 6 * kS
 // scheduler), the Original path HBM-bound either way.  The step's token (D1) is appended
 // by warp 0 before it waits for its first chunk.
 // ---------------------------------------------------------------------------------------
-constexpr int kChunkBytes = 12288;
+// chunk (stage) bytes: an 8 KB half Original tile or two 4.5 KB Quantized tiles.  (Measured:
+// 9 KB chunks, an idle 5th warp or no minimum-blocks bound leave the kernel time unchanged;
+// with any of them ~10 % of the first wave's CTAs start only when a CTA of the first wave
+// finishes — a dispatch effect we could not remove.)
+template <int C>
+constexpr int chunk_bytes() { return 12288; }
 template <int C>
 struct Smem3 {
   static constexpr int kStages = 2 * C;
+  static constexpr int kChunkBytes = chunk_bytes<C>();
   uint8_t ring[kStages][kChunkBytes];
   uint64_t full[kStages];
   float wm[C][8];
@@ -1088,8 +1094,7 @@ struct Smem3 {
 };
 
 template <int G, int NG, bool F8, int C>
-__global__ void __launch_bounds__(C * 32, C == 3 ? 3 : 2) decode_chunk_kernel(DecodeArgs a,
-                                                                              const __grid_constant__ UnitOrder cl) {
+__global__ void __launch_bounds__(C * 32, 2) decode_chunk_kernel(DecodeArgs a, const __grid_constant__ UnitOrder cl) {
 #ifdef ARKV_TUNING_KNOBS
   const unsigned long long t_start = gtimer();
 #endif
@@ -1128,7 +1133,7 @@ __global__ void __launch_bounds__(C * 32, C == 3 ? 3 : 2) decode_chunk_kernel(De
   if (a.nsplit && s == 0 && threadIdx.x == 0) a.nsplit[u] = S;  // for the combine
   const int o0 = (int)((int64_t)s * tiles_o / S), o1 = (int)((int64_t)(s + 1) * tiles_o / S);
   const int q0 = (int)((int64_t)s * tiles_q / S), q1 = (int)((int64_t)(s + 1) * tiles_q / S);
-  const int q_per = max(1, kChunkBytes / g.tile_q);  // Quantized tiles per chunk (int4: 2 x 4.5 KB; fp8: 1)
+  const int q_per = max(1, chunk_bytes<C>() / g.tile_q);  // Quantized tiles per chunk (int4: 2 x 4.5 KB; fp8: 1)
   const int n_oi = o1 - o0, n_qi = (q1 - q0 + q_per - 1) / q_per;
   const int n_work = n_oi + n_qi;
   const bool rev = a.item_order == 2 || (a.item_order == 1 && ((s + ul) & 1));
@@ -1334,7 +1339,7 @@ __global__ void __launch_bounds__(C * 32, C == 3 ? 3 : 2) decode_chunk_kernel(De
   // ---- CTA merge of the warps (+ the appended token) -> split partial ----
   const float* ob = (const float*)sm.ring[0];
   float* part = a.partials + ((int64_t)u * a.max_splits + s) * G * (D + 2);
-  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < G * D; idx += C * 32) {
     const int h = idx / D, x = idx % D;
     const int gr = x / (D / NG);
     float M = -INFINITY;
@@ -1395,8 +1400,20 @@ static void launch_chunk(const DecodeArgs& a, int n_units_call, cudaStream_t s, 
   }();
   const dim3 grid = cl ? dim3(cl->n_ctas) : dim3(a.n_splits, n_units_call);
   auto kern = decode_chunk_kernel<G, NG, F8, C>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static const bool once = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    carveout_max(kern);
+    return true;
+  }();
+  (void)once;
   if (ev0) cudaEventRecord(ev0, s);
+#ifdef ARKV_TUNING_KNOBS
+  if (tuning_knob("ARKV_DECODE_NOPDL", 0)) {
+    kern<<<grid, dim3(C * 32), (size_t)smem, s>>>(a, cl ? *cl : uniform);
+    if (ev1) cudaEventRecord(ev1, s);
+    return;
+  }
+#endif
   launch_pdl(kern, grid, dim3(C * 32), (size_t)smem, s, a, cl ? *cl : uniform);
   if (ev1) cudaEventRecord(ev1, s);
 }
@@ -1429,16 +1446,15 @@ static void launch_cfg(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
 template <int G, int NG>
 static void launch_gn(const DecodeArgs& a, int n_units_call, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
                       const UnitOrder* cl) {
-  // 3: chunked, 3 warps x 3 CTAs/SM; 4: chunked, 4 warps x 2 CTAs/SM; 2: producer ring
+  // 4: chunked, 4 warps x 2 CTAs/SM (12 KB chunks); 2: the producer-ring kernel.  (3 warps x
+  // 3 CTAs/SM measured 25 % slower, and 5 warps x 2 CTAs/SM with 9 KB chunks compiles to the
+  // same 168 registers with spills: register files are allocated in multi-warp units; 8 warps
+  // x 1 CTA/SM with 2, 3 or 4 CTAs per SM per step: 1-6 % slower.)
   static const int pipe = tuning_knob("ARKV_FAST_PIPE", 4);
-  if (pipe == 3 || pipe == 4) {
+  if (pipe == 4) {
     const bool f8 = a.g.mode == ARKV_QUANT_FP8;
-    if (pipe == 3)
-      f8 ? launch_chunk<G, NG, true, 3>(a, n_units_call, s, ev0, ev1, cl)
-         : launch_chunk<G, NG, false, 3>(a, n_units_call, s, ev0, ev1, cl);
-    else
-      f8 ? launch_chunk<G, NG, true, 4>(a, n_units_call, s, ev0, ev1, cl)
-         : launch_chunk<G, NG, false, 4>(a, n_units_call, s, ev0, ev1, cl);
+    f8 ? launch_chunk<G, NG, true, 4>(a, n_units_call, s, ev0, ev1, cl)
+       : launch_chunk<G, NG, false, 4>(a, n_units_call, s, ev0, ev1, cl);
     return;
   }
   if (a.g.mode == ARKV_QUANT_FP8) {
@@ -1942,6 +1958,16 @@ int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
 #ifdef ARKV_TUNING_KNOBS
 // on >= 0: enable/disable recording; out != nullptr: copy n records (8 x u64 each: start, end,
 // smid << 32 | unit * 64 + split, O tiles << 32 | Q tiles, first item staged, warp 0..2 done).
+extern "C" int arkv_debug_occupancy(int which) {
+  int nb = -1;
+  if (which == 0)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, arkv::fast::decode_chunk_kernel<4, 1, false, 4>, 128,
+                                                  sizeof(arkv::fast::Smem3<4>));
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, arkv::fast::decode_fast_kernel<4, 1, 3, 2, false>, 128,
+                                                  sizeof(arkv::fast::Smem<3, 2>));
+  return nb;
+}
 extern "C" int arkv_debug_cta_times(int on, unsigned long long* out, int n) {
   if (on >= 0) cudaMemcpyToSymbol(arkv::fast::g_cta_on, &on, sizeof(int));
   if (out) {

@@ -207,6 +207,15 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Keeps an SM's shared-memory carveout at its maximum for this kernel.  Kernels that run
+// between decode launches with a smaller carveout (the combines) left SMs configured so that
+// only one 100 KB decode CTA fit until they drained (timeline at configs[1]: 33 of 148 SMs
+// with one CTA for the first 40 % of the kernel).
+template <typename K>
+inline void carveout_max(K kern) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+}
+
 // k_decode_fast.cu: true when the tensor-core decode kernel supports this cache.
 bool decode_fast_available(const Geom& g);
 // k_decode_fast.cu: DecodeArgs::pscale of the fast kernels.

@@ -39,6 +39,7 @@ def main():
     lib = A.lib()
     fn = lib.arkv_debug_cta_times
     fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+    print("occupancy (blocks/SM): chunk kernel", lib.arkv_debug_occupancy(0), "ring kernel", lib.arkv_debug_occupancy(1))
     sh = Shape(batch=B, n_layers=L, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, prompt_len=P, window=wl["window"])
     qw, k, v = prefill_inputs_fast(sh, seed=1234, device=dev)
     rho_ov = None
