@@ -488,15 +488,17 @@ __device__ __forceinline__ void qk_softmax(const uint8_t* tb, bool isq, int n_va
       }
     }
   }
-  // mask rows beyond the segment (and padding heads)
+  // mask rows beyond the segment (only the last tile of a segment is partial).  Padding
+  // heads (h >= G, columns of lanes tq >= G/2) are not masked: their logits are 0 (zero q
+  // fragments), and no padding column enters the PV operand (make_b), the HH logits or the
+  // merged statistics.
+  if (n_valid < kTile) {
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int j = mt * 16 + gq + 8 * (e >> 1);
-      const int h = 2 * tq + (e & 1);
-      if (j >= n_valid || h >= G) lg[mt][e] = -INFINITY;
-    }
+      for (int e = 0; e < 4; ++e)
+        if (mt * 16 + gq + 8 * (e >> 1) >= n_valid) lg[mt][e] = -INFINITY;
+  }
   if (lrow) {
     // logits [row][G]: this lane's heads 2t, 2t+1 of a row are adjacent — one 8-byte store
     // per (m-tile, row half); the 8 rows x G heads of one store instruction are contiguous
@@ -634,13 +636,14 @@ __device__ __forceinline__ void pv_quant(const uint8_t* tb, const float (&p)[2][
     for (int kc = 0; kc < 2; ++kc) {
 #pragma unroll
       for (int gr = 0; gr < NG; ++gr) {
-        float vsc[2];
+        float vsc[2];  // v_scale (x 2^24: subnormal codes) x 1/16 for the odd-nibble rows g+8
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh)
-          vsc[hh] = sc[((kc * 16 + gq + 8 * hh) * NG + gr) * 4 + 2] * (kPvSub ? kSubScale : 1.f);
+          vsc[hh] = sc[((kc * 16 + gq + 8 * hh) * NG + gr) * 4 + 2] *
+                    ((kPvSub ? kSubScale : 1.f) * (hh ? 0.0625f : 1.f));
         float pv[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) pv[e] = p[kc][e] * vsc[e >> 1] * ((e >> 1) ? 0.0625f : 1.f);
+        for (int e = 0; e < 4; ++e) pv[e] = p[kc][e] * vsc[e >> 1];
         make_b<G, false>(pv, tq, b01[gr][kc], b23[gr][kc], c01[gr][kc], c23[gr][kc]);
         // zero-point term Σ p·z_v
 #pragma unroll
@@ -1166,48 +1169,44 @@ __global__ void __launch_bounds__(C * 32, 2) decode_chunk_kernel(DecodeArgs a, c
   __syncwarp();
   const uint64_t lpol = l2_evict_last();  // HH logits stay in L2 for the combine
   const uint64_t pol_stream = l2_evict_first();
-  // the warp's chunk cursor: (item, part); part 1 = the V^T block of an Original tile
+  // the warp's chunk cursor: (item, part; the item's kind and tiles); part 1 = the V^T block
+  // of an Original tile.  The item is decoded once, when the cursor reaches it.
   struct Cur {
     int i, part;
-  };
-  auto chunk_src = [&](const Cur& c, const uint8_t*& src, uint32_t& bytes) {
     bool isq;
     int first, ntiles;
-    item_of(c.i, isq, first, ntiles);
-    if (isq) {
-      src = q_tile_ptr(slot, g, first + ntiles - 1);
-      bytes = (uint32_t)(ntiles * g.tile_q);
-    } else {
-      src = o_tile_ptr(slot, g, first) + (c.part ? 64 * D : 0);
-      bytes = (uint32_t)(32 * D * 2);
+  };
+  auto make_cur = [&](int i) {
+    Cur c{i, 0, false, 0, 0};
+    if (i < n_work) item_of(i, c.isq, c.first, c.ntiles);
+    return c;
+  };
+  auto next = [&](const Cur& c) {
+    if (!c.isq && c.part == 0) {
+      Cur d = c;
+      d.part = 1;
+      return d;
     }
-  };
-  auto next = [&](Cur c) {
-    bool isq;
-    int first, ntiles;
-    item_of(c.i, isq, first, ntiles);
-    if (!isq && c.part == 0) return Cur{c.i, 1};
-    return Cur{c.i + C, 0};
+    return make_cur(c.i + C);
   };
   auto issue = [&](const Cur& c, int st) {  // lane 0
-    const uint8_t* src;
-    uint32_t bytes;
-    chunk_src(c, src, bytes);
+    const uint8_t* src = c.isq ? q_tile_ptr(slot, g, c.first + c.ntiles - 1)
+                               : o_tile_ptr(slot, g, c.first) + (c.part ? 64 * D : 0);
+    const uint32_t bytes = c.isq ? (uint32_t)(c.ntiles * g.tile_q) : (uint32_t)(32 * D * 2);
     mbar_expect_tx(&sm.full[st], bytes);
     if (a.l2_hints)
       bulk_g2s_hint(sm.ring[st], src, bytes, &sm.full[st], pol_stream);
     else
       bulk_g2s(sm.ring[st], src, bytes, &sm.full[st]);
   };
-  Cur fetch{warp, 0};
+  Cur fetch = make_cur(warp);
   if (lane == 0) {
     for (int k = 0; k < 2 && fetch.i < n_work; ++k) {
       issue(fetch, 2 * warp + k);
       fetch = next(fetch);
     }
   }
-  fetch = Cur{warp, 0};
-  fetch = next(next(fetch));  // every lane tracks the cursor (lane 0 issued the first two)
+  fetch = next(next(make_cur(warp)));  // every lane tracks the cursor (lane 0 issued the first two)
   if (warp == 0 && owns_new) {
     // the step's token (D1): appended while the first chunks are in flight
     if (warp_step_nonfinite(qp, G * D, kn, vn, D, lane) && lane == 0) atomicOr(a.err, kErrNonFinite);
@@ -1252,7 +1251,7 @@ __global__ void __launch_bounds__(C * 32, 2) decode_chunk_kernel(DecodeArgs a, c
   const int src_lane = (lane & ~3) | src_t;
   float p[2][4];        // an Original tile's probabilities, from its K chunk to its V chunk
   int o_valid = kTile;  // ... and its rows in use
-  Cur cur{warp, 0};
+  Cur cur = make_cur(warp);
   uint32_t ph = 0;
   int k = 0;
 #ifdef ARKV_TUNING_KNOBS
@@ -1269,9 +1268,8 @@ __global__ void __launch_bounds__(C * 32, 2) decode_chunk_kernel(DecodeArgs a, c
     }
     first_chunk = false;
 #endif
-    bool isq;
-    int first, ntiles;
-    item_of(cur.i, isq, first, ntiles);
+    const bool isq = cur.isq;
+    const int first = cur.first, ntiles = cur.ntiles;
     const uint8_t* tb = sm.ring[st];
     if (isq) {
       for (int jt = 0; jt < ntiles; ++jt) {

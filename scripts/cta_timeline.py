@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--at", type=int, nargs="+", default=[10, 40])
     ap.add_argument("--mode", default="arkv")
     ap.add_argument("--dump", default=".")
+    ap.add_argument("--per-layer", action="store_true",
+                    help="one call per layer; the recorded call is layer L/2 of each --at step, also timed with events")
     args = ap.parse_args()
     wl = bench.WORKLOADS[args.workload]
     B, L, Hq, Hkv, d, P = (wl["batch"], wl["n_layers"], wl["n_q_heads"], wl["n_kv_heads"], wl["head_dim"],
@@ -56,10 +58,32 @@ def main():
         if rec:
             torch.cuda.synchronize()
             fn(1, None, 0)
-        cache.arkv_decode_step(q, kk, vv, out=out)
+        if args.per_layer:
+            lr = L // 2
+            for l in range(L):
+                ql, kl, vl = q[:, l:l + 1].contiguous(), kk[:, l:l + 1].contiguous(), vv[:, l:l + 1].contiguous()
+                if rec and l == lr:
+                    torch.cuda.synchronize()
+                    fn(1, None, 0)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    cache.arkv_decode_step(ql, kl, vl, layer0=l, out=out[:, l:l + 1])
+                    e1.record()
+                    torch.cuda.synchronize()
+                    print(f"   layer call {l} at step {s}: {e0.elapsed_time(e1) * 1e3:.1f} us (events)")
+                    fn(0, ctypes.cast(buf, ctypes.c_void_p), n_max)
+                    break
+                cache.arkv_decode_step(ql, kl, vl, layer0=l, out=out[:, l:l + 1].contiguous())
+            if rec:
+                for l in range(lr + 1, L):
+                    ql, kl, vl = q[:, l:l + 1].contiguous(), kk[:, l:l + 1].contiguous(), vv[:, l:l + 1].contiguous()
+                    cache.arkv_decode_step(ql, kl, vl, layer0=l, out=out[:, l:l + 1].contiguous())
+        else:
+            cache.arkv_decode_step(q, kk, vv, out=out)
         if rec:
             torch.cuda.synchronize()
-            fn(0, ctypes.cast(buf, ctypes.c_void_p), n_max)
+            if not args.per_layer:
+                fn(0, ctypes.cast(buf, ctypes.c_void_p), n_max)
             r = np.frombuffer(buf, dtype=np.uint64).reshape(n_max, 8).copy()
             fn(0, None, 0)
             valid = r[:, 1] > 0
@@ -85,6 +109,9 @@ def main():
             by = n_ot * 16384 + n_qt * 4608
             print(f"== step {s}: {len(r)} CTAs, kernel span {span / 1e3:.1f} us, "
                   f"bytes {by.sum() / 1e6:.1f} MB -> {by.sum() / span:.0f} GB/s over the span")
+            if len(r) < 400:
+                print(f"   CTA durations (us): min {dur.min() / 1e3:.1f} median {np.median(dur) / 1e3:.1f} max {dur.max() / 1e3:.1f}; "
+                      f"fill mean {np.mean(r[:, 4].astype(np.int64) - base - t0) / 1e3:.1f}")
             busy = np.zeros(sm.max() + 1)
             last = np.zeros(sm.max() + 1)
             for i in range(len(r)):
