@@ -365,7 +365,7 @@ def run_arkv(args, wl):
     value = Bg * K / (ms / 1e3)
     kernel_ms = k_ms / max(k_cnt, 1)
     achieved = (k_by / max(k_cnt, 1)) / (kernel_ms / 1e3) / 1e9 if k_cnt else None
-    tp = traffic_record(args, kind)
+    tp = traffic_record(args, kind, "hh_window" if args.warmup + K <= wl["window"] else "steady")
     pf = np.median(np.array(run.prefill_ms), axis=0)
     P = wl["prompt_len"]
     k_pass_bytes = 2.0 * run.B * L * run.Hkv * P * d * 2  # K read once per pass (P1 algorithmic bytes)
@@ -596,20 +596,24 @@ def read_ceiling_gbs(dev) -> float:
 
 def cache_kernel(cache) -> str:
     from paper_2603_08727_b200 import arkv as A
-    return {0: "generic", 1: "split-K", 2: "persistent",
-            3: "auto (split-K; persistent when >= 60% of a call's bytes are Quantized tiles)"}[
+    return {0: "generic", 1: "split-K (chunked pipeline, cost-balanced LPT splits)", 2: "persistent",
+            3: "auto (split-K chunked pipeline with cost-balanced LPT splits; persistent at >= 32 units per SM)"}[
         A.lib().arkv_cache_info(cache.handle, 1)]
 
 
-def traffic_record(args, kind):
+def traffic_record(args, kind, window):
     """ncu DRAM bytes per launch of the decode kernel (profiles/ncu_traffic.json), with the
-    capture it came from; the library cannot read DRAM counters in-process."""
+    capture it came from; the library cannot read DRAM counters in-process.  window:
+    "hh_window" when the timed steps all lie in the first heavy-hitter window after the prompt
+    (caches at their fullest, logit stores), else "steady"."""
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if args.mode != "arkv" or not os.path.exists(tp):
         return None
     try:
         rec = json.load(open(tp)).get(args.workload, {}).get(kind)
-        return rec if isinstance(rec, dict) else None
+        if isinstance(rec, dict) and window in rec:
+            rec = rec[window]
+        return rec if isinstance(rec, dict) and "dram_bytes_per_launch" in rec else None
     except Exception:
         return None
 

@@ -266,7 +266,7 @@ bool check_cuda(cudaError_t e) {
 extern "C" {
 
 const char* arkv_version(void) {
-  return "arkv 0.4 sm_100a layouts=plain,frag decode=generic,mma-sync-split,mma-sync-persistent "
+  return "arkv 0.5 sm_100a layouts=plain,frag decode=generic,mma-sync-chunked-split,mma-sync-persistent "
          "prefill=tcgen05-tma-ws,mma-sync quant=int2/4/8,fp8-e4m3 states=per-head,layer-shared "
          "scores=eq9,smoothed";
 }
