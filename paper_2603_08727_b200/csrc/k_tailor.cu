@@ -618,7 +618,7 @@ struct Smem {
 }  // namespace mvf
 
 template <int NG>
-__global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, TailorJobs jobs, uint8_t* slots,
+__global__ void __launch_bounds__(256, 6) tailor_move_frag_kernel(Geom g_in, TailorJobs jobs, uint8_t* slots,
                                                                uint8_t* meta, const uint16_t* __restrict__ pk,
                                                                const uint16_t* __restrict__ pv, int P,
                                                                const int32_t* __restrict__ src_scratch,
@@ -687,19 +687,29 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
     }
   }
   // ---- phase 1: one warp per row.  The warp's prompt rows (the prefill-end tailor's only
-  // source) are all loaded first: one row in flight per warp left the kernel waiting on
-  // these loads (ncu: 35 % of the stall samples at their first use) ----
-  uint4 pre[RPW];
+  // source) are first copied into the staging rows with cp.async, all kTile / 8 in flight
+  // at once and no registers held (ncu: with one row load in flight per warp, 35 % of the
+  // stall samples waited on it; loading them into registers instead measured slower, 57
+  // instead of 40 registers) ----
+  {
+    bool any = false;
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int32_t sref = __shfl_sync(0xffffffffu, my_sref, r);
-    pre[r] = make_uint4(0u, 0u, 0u, 0u);
-    if (tid * kTile + warp + 8 * r < n_new && (sref >> 28) == kSrcInput)
-      pre[r] = *(const uint4*)((lane < 16 ? upk : upv) + (int64_t)(sref & 0x0FFFFFFF) * D + (lane & 15) * 8);
+    for (int r = 0; r < RPW; ++r) {
+      const int32_t sref = __shfl_sync(0xffffffffu, my_sref, r);
+      const int j = warp + 8 * r;
+      if (tid * kTile + j < n_new && (sref >> 28) == kSrcInput) {
+        const uint16_t* rowp = (lane < 16 ? upk : upv) + (int64_t)(sref & 0x0FFFFFFF) * D + (lane & 15) * 8;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&sm.stage[lane >> 4][j][(lane & 15) * 8])),
+                     "l"(rowp)
+                     : "memory");
+        any = true;
+      }
+    }
+    if (any) asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
   }
-#pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int j = warp + 8 * r;
+  for (int j = warp, r = 0; j < kTile; j += 8, ++r) {
     const int row = tid * kTile + j;
     const int32_t sref = __shfl_sync(0xffffffffu, my_sref, r);
     if (row >= n_new) {  // rows past the segment: zeros (defined bytes; masked by the readers)
@@ -731,9 +741,8 @@ __global__ void __launch_bounds__(256) tailor_move_frag_kernel(Geom g_in, Tailor
         sm.stage[1][j][x] = f_to_bf16_rne(__fadd_rn(__fmul_rn((float)cv, s4.z), s4.w));
       }
     } else if (kind == kSrcInput) {
-      // prompt row: 16 lanes x 16 B of K, 16 lanes x 16 B of V (loaded above)
-      const uint4 pr = pre[r];
-      *(uint4*)&sm.stage[lane >> 4][j][(lane & 15) * 8] = pr;
+      // prompt row: 16 lanes x 16 B of K, 16 lanes x 16 B of V, staged above
+      const uint4 pr = *(const uint4*)&sm.stage[lane >> 4][j][(lane & 15) * 8];
       nonfinite_bits |= bf16x8_expmax_bits(pr);  // prompt values entering the cache
     } else {
       // old Original row: K quad (t, q) holds dims 32t + 8q .. +7 of the token (FRAG K map)
