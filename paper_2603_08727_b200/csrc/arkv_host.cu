@@ -60,6 +60,7 @@ struct arkv_cache {
   int32_t* counters = nullptr;
   int32_t* nsplit = nullptr;
   std::unique_ptr<UnitOrder> chunks{new UnitOrder};  // split-K launch order (host copy, a kernel parameter)
+  std::vector<int> chunk_ns;                          // its split count per (sequence, layer) of the call
   // persistent decode kernel (decode_kernel = 3): partial slots and coverage tables
   float* pparts = nullptr;
   int4* pcta = nullptr;
@@ -1070,6 +1071,7 @@ static bool build_chunks(arkv_cache* c, int layer0, int n_layers, int slots) {
   uo.pfx[pos] = (uint16_t)cta;
   uo.n_units = pos;
   uo.n_ctas = cta;
+  c->chunk_ns.assign(ns.begin(), ns.end());
   return true;
 }
 
@@ -1205,6 +1207,10 @@ arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, co
   if (!persist && c->fast && build_chunks(c, layer0, n_layers, slots)) {
     pa.chunks = c->chunks.get();
     pa.nsplit = c->nsplit;
+    // the HH combine merges each unit's partials with the split count known here
+    for (int k = 0; k < hh.n; ++k) hh.e[k].z |= c->chunk_ns[hh.e[k].x] << 1;
+  } else {
+    for (int k = 0; k < hh.n; ++k) hh.e[k].z |= S << 1;
   }
   if (persist) {
     build_plan(c, layer0, n_layers, 2 * c->num_sms, &plan);

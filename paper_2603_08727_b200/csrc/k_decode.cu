@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(kHhRowsPerThread == 8 ? 256 : 1024) decode_com
   const int n_rows = en.y, r0 = (cg - hp.coff[lo]) * R;
   const int b = en.x / a.n_layers, li = en.x % a.n_layers;
   const int u = (b * g.L + a.layer0 + li) * g.Hkv + kvh;
-  const bool first = en.z != 0;
+  const bool first = (en.z & 1) != 0;
+  const int S_hh = (en.z >> 1) > 0 ? (en.z >> 1) : a.n_splits;  // no dependent nsplit load
   const int n_o = n_rows - en.w;  // Original rows, the appended token included
   // the slot is not changed by the combine's descriptor advance
   const SlotMeta sm = slot_meta(a.meta, g, a.desc[u].slot);
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(kHhRowsPerThread == 8 ? 256 : 1024) decode_com
     if (lane < G) {
       const float* part = a.partials + (int64_t)u * a.max_splits * G * (g.d + 2);
       float M, L, O;
-      merge_splits<G, false>(part, lane, 0, a.nsplit ? a.nsplit[u] : a.n_splits, g.d, M, L, O);
+      merge_splits<G, false>(part, lane, 0, S_hh, g.d, M, L, O);
       mh = M;
       ilh = 1.0f / L;
     }

@@ -151,7 +151,8 @@ struct HhPlan {
   int n_chunks;    // row chunks of all entries (HH blocks = n_chunks x H_kv)
   int pad_;
   int4 e[kMaxHhEntries];  // x = b * n_layers + li; y = rows (n_o after the append + n_q);
-                          // z = 1 on the window's first step (acc := sample); w = n_q
+                          // z = bit 0: the window's first step (acc := sample), bits 1..:
+                          // the entry's split count this step (0: n_splits); w = n_q
   int coff[kMaxHhEntries + 1];  // first chunk of each entry (its own row count: no empty blocks)
 };
 // Split-K launch order of the fast decode kernel ("cost-balanced splits").
