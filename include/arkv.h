@@ -231,6 +231,21 @@ arkv_status arkv_set_tailor_scores(arkv_cache* cache, const float* d_scores, int
 arkv_status arkv_persist_plan_check(const arkv_config* cfg, const int32_t* n_o, const int32_t* n_q,
                                     int32_t n_units, int32_t max_ctas, int32_t* ctas_used);
 
+/* Host only.  Builds the split-K decode kernel's cost-balanced launch order (DESIGN.md §6,
+   "cost-balanced split-K launch order") for n_pairs (sequence, layer) pairs of a call with
+   the given Original rows before the step's append (n_o) and Quantized rows (n_q), each
+   pair with the cache's H_kv KV heads, on a GPU of num_sms SMs (2 CTAs per SM), then
+   replays what the kernel derives from it: every unit of the call exactly once, each
+   unit's split count in 1 .. max_splits and equal for the KV heads of a pair, the kernel's
+   split ranges covering each unit's Original and Quantized tiles exactly once, at most
+   2 x 2 num_sms CTAs plus one per unit whose cost share rounds to zero, and pieces in
+   non-increasing estimated cost (LPT).  *n_ctas = the
+   grid.  ARKV_ERR_DEVICE on a violated invariant, ARKV_ERR_CAPACITY when the call has more
+   units than the order holds (the kernel then uses its uniform grid),
+   ARKV_ERR_INVALID_ARG on counts outside the cache's capacity. */
+arkv_status arkv_split_order_check(const arkv_config* cfg, const int32_t* n_o, const int32_t* n_q, int32_t n_pairs,
+                                   int32_t num_sms, int32_t* n_ctas);
+
 /* Host only.  Statistics -> OQ score (Eq. 6 with the R6 clamps applied to the raw
    moments). */
 arkv_status arkv_oq_score(const arkv_config* cfg, double entropy, double m2, double m4, double* stats3,

@@ -51,7 +51,7 @@ EXPORTED = [
     "arkv_check", "arkv_schedule", "arkv_oq_score", "arkv_launch_count", "arkv_version",
     "arkv_status_string", "arkv_cache_info", "arkv_prefill_begin", "arkv_prefill_finish",
     "arkv_profile", "arkv_profile_read", "arkv_layout_check", "arkv_persist_plan_check",
-    "arkv_tailor_scores", "arkv_set_tailor_scores",
+    "arkv_tailor_scores", "arkv_set_tailor_scores", "arkv_split_order_check",
 ]
 
 _lib = None
@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
         L.arkv_oq_score.argtypes = [P(ArkvConfig), dbl, dbl, dbl, P(dbl), P(dbl)]
         L.arkv_layout_check.argtypes = [P(ArkvConfig), P(ctypes.c_int64)]
         L.arkv_persist_plan_check.argtypes = [P(ArkvConfig), P(i32), P(i32), i32, i32, P(i32)]
+        L.arkv_split_order_check.argtypes = [P(ArkvConfig), P(i32), P(i32), i32, i32, P(i32)]
         L.arkv_tailor_scores.argtypes = [vp, i32, i32, vp, ctypes.c_int64, i32, P(i32), vp]
         L.arkv_set_tailor_scores.argtypes = [vp, vp, ctypes.c_int64, i32]
         L.arkv_cache_info.argtypes = [vp, i32]
@@ -158,6 +159,19 @@ def arkv_persist_plan_check(cfg: ArkvConfig, n_o, n_q, max_ctas: int) -> int:
     used = ctypes.c_int32()
     _ok(lib().arkv_persist_plan_check(ctypes.byref(cfg), a, b, n, max_ctas, ctypes.byref(used)),
         "arkv_persist_plan_check")
+    return used.value
+
+
+def arkv_split_order_check(cfg: ArkvConfig, n_o, n_q, num_sms: int = 148) -> int:
+    """Builds the split-K decode kernel's cost-balanced launch order for these per-(sequence,
+    layer) counts and replays it on the host (include/arkv.h); raises ArkvError on a violated
+    invariant.  Returns the grid size."""
+    n = len(n_o)
+    a = (ctypes.c_int32 * n)(*[int(x) for x in n_o])
+    b = (ctypes.c_int32 * n)(*[int(x) for x in n_q])
+    used = ctypes.c_int32()
+    _ok(lib().arkv_split_order_check(ctypes.byref(cfg), a, b, n, num_sms, ctypes.byref(used)),
+        "arkv_split_order_check")
     return used.value
 
 

@@ -931,6 +931,56 @@ arkv_status arkv_persist_plan_check(const arkv_config* cfg, const int32_t* n_o, 
   return ok ? ARKV_OK : ARKV_ERR_DEVICE;
 }
 
+static bool order_from_counts(const Geom& g, int BL, const int32_t* n_o, const int32_t* n_q, int max_splits,
+                              int slots, UnitOrder& uo, std::vector<int>& ns);
+
+arkv_status arkv_split_order_check(const arkv_config* cfg, const int32_t* n_o, const int32_t* n_q, int32_t n_pairs,
+                                   int32_t num_sms, int32_t* n_ctas) {
+  arkv_status st = validate(cfg);
+  if (st != ARKV_OK) return st;
+  if (!n_o || !n_q || n_pairs <= 0 || num_sms <= 0) return ARKV_ERR_INVALID_ARG;
+  Sizes s = compute_sizes(*cfg);
+  const Geom& g = s.g;
+  if (n_pairs > g.batch * g.L) return ARKV_ERR_INVALID_ARG;
+  for (int i = 0; i < n_pairs; ++i)
+    if (n_o[i] < 0 || n_q[i] < 0 || n_o[i] >= g.cap_o || n_q[i] > g.cap_q) return ARKV_ERR_INVALID_ARG;
+  std::unique_ptr<UnitOrder> uo(new UnitOrder);
+  std::vector<int> ns;
+  const int slots = 2 * num_sms;
+  if (!order_from_counts(g, n_pairs, n_o, n_q, s.max_splits, slots, *uo, ns)) return ARKV_ERR_CAPACITY;
+  if (n_ctas) *n_ctas = uo->n_ctas;
+  // replay what the decode kernel derives from the order: every unit exactly once, its
+  // splits [pfx[p], pfx[p + 1]) in 1 .. max_splits, every Original and Quantized tile of
+  // the unit in exactly one split, and the positions in non-increasing piece cost
+  const int n_units = n_pairs * g.Hkv;
+  if (uo->n_units != n_units || uo->pfx[0] != 0 || uo->pfx[n_units] != uo->n_ctas) return ARKV_ERR_DEVICE;
+  std::vector<int> seen(n_units, 0);
+  // the apportionment targets 2 CTAs per slot; a pair whose share rounds to 0 still gets one
+  const int64_t want = (std::max<int64_t>(n_pairs, (int64_t)2 * slots / g.Hkv) + n_pairs) * g.Hkv;
+  if (uo->n_ctas > want) return ARKV_ERR_DEVICE;
+  double prev = INFINITY;
+  for (int p = 0; p < n_units; ++p) {
+    const int ul = uo->perm[p], S = uo->pfx[p + 1] - uo->pfx[p];
+    if (ul < 0 || ul >= n_units || seen[ul]++ || S < 1 || S > s.max_splits || S != ns[ul / g.Hkv])
+      return ARKV_ERR_DEVICE;
+    const int i = ul / g.Hkv;
+    const int to = (n_o[i] + 1 + kTile - 1) / kTile, tq = (n_q[i] + kTile - 1) / kTile;
+    const double piece = (to + 0.01 * tuning_knob("ARKV_QCOST", 62) * tq) / S;
+    if (piece > prev + 1e-9) return ARKV_ERR_DEVICE;
+    prev = piece;
+    int o_next = 0, q_next = 0;
+    for (int sp = 0; sp < S; ++sp) {  // the kernel's split ranges (k_decode_fast.cu)
+      const int o0 = (int)((int64_t)sp * to / S), o1 = (int)((int64_t)(sp + 1) * to / S);
+      const int q0 = (int)((int64_t)sp * tq / S), q1 = (int)((int64_t)(sp + 1) * tq / S);
+      if (o0 != o_next || q0 != q_next || o1 < o0 || q1 < q0) return ARKV_ERR_DEVICE;
+      o_next = o1;
+      q_next = q1;
+    }
+    if (o_next != to || q_next != tq) return ARKV_ERR_DEVICE;
+  }
+  return ARKV_OK;
+}
+
 arkv_status arkv_tailor_scores(arkv_cache* c, int32_t layer0, int32_t n_layers, float* d_scores, int64_t stride,
                                int32_t max_rows, int32_t* n_rows, void* stream) {
   if (!c || !d_scores || !n_rows) return ARKV_ERR_INVALID_ARG;
@@ -1017,27 +1067,25 @@ arkv_status arkv_set_tailor_scores(arkv_cache* c, const float* d_scores, int64_t
 // per-unit cap of ~min_items work items per CTA and max_splits), and the units are launched
 // in decreasing piece cost (LPT).  Measured at configs[1]: HH-window decode kernel -6 %,
 // steady state -1 % (2 waves beat 3 and 4: fewer per-CTA fills and drains).
-static bool build_chunks(arkv_cache* c, int layer0, int n_layers, int slots) {
-  const Geom& g = c->g;
-  const int n_units = g.batch * n_layers * g.Hkv;
-  static const int mode = tuning_knob("ARKV_CHUNKS", 1);  // 0: the uniform grid
-  if (mode == 0 || n_units > kMaxOrderUnits) return false;
+// The order for BL (sequence, layer) pairs with counts n_o (before this step's append) and
+// n_q, each with g.Hkv KV heads (units i * Hkv + kvh).  ns: split count per pair.
+static bool order_from_counts(const Geom& g, int BL, const int32_t* n_o, const int32_t* n_q, int max_splits,
+                              int slots, UnitOrder& uo, std::vector<int>& ns) {
+  if (BL * g.Hkv > kMaxOrderUnits) return false;
   static const double q_cost = 0.01 * tuning_knob("ARKV_QCOST", 62);
   static const int waves = tuning_knob("ARKV_EXACT_WAVES", 2);
   static const int min_items = tuning_knob("ARKV_MIN_ITEMS", 20);
-  const int BL = g.batch * n_layers;
   std::vector<double> cost(BL), x(BL);
-  std::vector<int> cap(BL), ns(BL);
+  std::vector<int> cap(BL);
+  ns.assign(BL, 1);
   double total = 0.0;
-  for (int b = 0; b < g.batch; ++b)
-    for (int l = layer0; l < layer0 + n_layers; ++l) {
-      const int bl = b * g.L + l, i = b * n_layers + (l - layer0);
-      const int to = (c->n_o[bl] + 1 + kTile - 1) / kTile, tq = (c->n_q[bl] + kTile - 1) / kTile;
-      cost[i] = to + q_cost * tq;
-      const int items = to + (tq + 2) / 3;
-      cap[i] = std::max(1, std::min({c->max_splits, to + tq, items / std::max(1, min_items), 0xFFFF}));
-      total += cost[i];
-    }
+  for (int i = 0; i < BL; ++i) {
+    const int to = (n_o[i] + 1 + kTile - 1) / kTile, tq = (n_q[i] + kTile - 1) / kTile;
+    cost[i] = to + q_cost * tq;
+    const int items = to + (tq + 2) / 3;
+    cap[i] = std::max(1, std::min({max_splits, to + tq, items / std::max(1, min_items), 256}));
+    total += cost[i];
+  }
   // per (sequence, layer): every KV head of it has the same counts and the same split count
   const int64_t want = std::max<int64_t>(BL, (int64_t)waves * slots / g.Hkv);
   int64_t n = 0;
@@ -1057,7 +1105,6 @@ static bool build_chunks(arkv_cache* c, int layer0, int n_layers, int slots) {
   if (n * g.Hkv > 0xFFFF) return false;
   // launch order: decreasing piece cost (LPT), then unit index
   std::stable_sort(idx.begin(), idx.end(), [&](int p, int q) { return cost[p] / ns[p] > cost[q] / ns[q]; });
-  UnitOrder& uo = *c->chunks;
   int pos = 0, cta = 0;
   for (int j = 0; j < BL; ++j) {
     const int i = idx[j];
@@ -1071,8 +1118,21 @@ static bool build_chunks(arkv_cache* c, int layer0, int n_layers, int slots) {
   uo.pfx[pos] = (uint16_t)cta;
   uo.n_units = pos;
   uo.n_ctas = cta;
-  c->chunk_ns.assign(ns.begin(), ns.end());
   return true;
+}
+
+static bool build_chunks(arkv_cache* c, int layer0, int n_layers, int slots) {
+  static const int mode = tuning_knob("ARKV_CHUNKS", 1);  // 0: the uniform grid
+  if (mode == 0) return false;
+  const Geom& g = c->g;
+  const int BL = g.batch * n_layers;
+  std::vector<int32_t> no(BL), nq(BL);
+  for (int b = 0; b < g.batch; ++b)
+    for (int l = layer0; l < layer0 + n_layers; ++l) {
+      no[b * n_layers + (l - layer0)] = c->n_o[b * g.L + l];
+      nq[b * n_layers + (l - layer0)] = c->n_q[b * g.L + l];
+    }
+  return order_from_counts(g, BL, no.data(), nq.data(), c->max_splits, slots, *c->chunks, c->chunk_ns);
 }
 
 arkv_status arkv_decode_step(arkv_cache* c, int32_t layer0, int32_t n_layers, const void* q, const void* k,

@@ -187,3 +187,33 @@ def test_persist_plan_configs1_keeps_full_grid():
         n_o += [o] * 8
         n_q += [q] * 8
     assert A.arkv_persist_plan_check(c, n_o, n_q, 296) == 296
+
+
+@settings(max_examples=300, deadline=None)
+@given(n_layers=st.integers(1, 8), batch=st.integers(1, 3), hkv=st.sampled_from([1, 2, 8]),
+       num_sms=st.sampled_from([1, 8, 148]), data=st.data())
+def test_split_order_replay(n_layers, batch, hkv, num_sms, data):
+    """The split-K kernel's cost-balanced launch order (host C++), replayed on the host:
+    every unit once, split counts within bounds and equal across a pair's KV heads, the
+    kernel's split ranges tile each unit exactly, LPT order, at most 2 CTAs per slot."""
+    B = 2048
+    c = A.make_config(n_layers, 4 * hkv, hkv, 128, batch=batch, window=32, budget_tokens=B,
+                      max_positions=4 * B, layout=2)
+    n_pairs = batch * n_layers
+    counts = st.tuples(st.integers(0, B - 1), st.integers(0, 3 * B))
+    pairs = data.draw(st.lists(counts, min_size=n_pairs, max_size=n_pairs))
+    n_ctas = A.arkv_split_order_check(c, [p[0] for p in pairs], [p[1] for p in pairs], num_sms)
+    assert n_pairs * hkv <= n_ctas <= (max(n_pairs, 4 * num_sms // hkv) + n_pairs) * hkv
+
+
+def test_split_order_configs1_exact_waves():
+    """configs[1]-like counts (per-layer rho): exactly 2 CTAs per slot (2 x 296)."""
+    c = A.make_config(32, 32, 8, 128, window=32, budget_tokens=8192, max_positions=40000, layout=2)
+    rng = np.random.default_rng(0)
+    n_o, n_q = [], []
+    for _ in range(32):
+        rho = rng.uniform(0.05, 0.95)
+        o = int(rho * 8160) + 32
+        n_o.append(o)
+        n_q.append(int((8192 - o) * 512 / 144))
+    assert A.arkv_split_order_check(c, n_o, n_q, 148) == 592
