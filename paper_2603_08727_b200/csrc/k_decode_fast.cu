@@ -1956,6 +1956,11 @@ int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
 #ifdef ARKV_TUNING_KNOBS
 // on >= 0: enable/disable recording; out != nullptr: copy n records (8 x u64 each: start, end,
 // smid << 32 | unit * 64 + split, O tiles << 32 | Q tiles, first item staged, warp 0..2 done).
+extern "C" int arkv_debug_cta_clear() {
+  static unsigned long long zeros[arkv::fast::kCtaTimesMax][8] = {};
+  cudaMemcpyToSymbol(arkv::fast::g_cta_t, zeros, sizeof(zeros));
+  return (int)cudaGetLastError();
+}
 extern "C" int arkv_debug_occupancy(int which) {
   int nb = -1;
   if (which == 0)

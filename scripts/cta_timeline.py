@@ -65,6 +65,8 @@ def main():
                 if rec and l == lr:
                     torch.cuda.synchronize()
                     fn(1, None, 0)
+                    clr = lib.arkv_debug_cta_clear
+                    clr()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
                     cache.arkv_decode_step(ql, kl, vl, layer0=l, out=out[:, l:l + 1])
