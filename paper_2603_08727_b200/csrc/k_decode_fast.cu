@@ -1094,6 +1094,7 @@ struct Smem3 {
   float wl[C][8];
   float wz[C][8][4];
   float newtok[8];
+  int is_last;  // fused combine: this CTA is the last split of its unit to finish
 };
 
 template <int G, int NG, bool F8, int C>
@@ -1369,6 +1370,19 @@ __global__ void __launch_bounds__(C * 32, 2) decode_chunk_kernel(DecodeArgs a, c
     if (x == 0) {
       part[h * (D + 2) + 0] = M;
       part[h * (D + 2) + 1] = L;
+    }
+  }
+  // ---- fused combine (tuning builds, ARKV_FUSE_COMBINE): the last split CTA of the unit
+  // to finish merges all partials ----
+  if (a.fuse_combine) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) sm.is_last = atomicAdd(&a.counters[u], 1) == S - 1;
+    __syncthreads();
+    if (sm.is_last) {
+      __threadfence();
+      combine_unit<G>(a, u, b, li, kvh, dsc, nullptr, nullptr);
+      if (threadIdx.x == 0) a.counters[u] = 0;
     }
   }
 #ifdef ARKV_TUNING_KNOBS
@@ -1942,7 +1956,13 @@ int launch_decode_fast(const DecodeArgs& a, int n_units_call, cudaStream_t s, cu
     default: return -1;
   }
   if (r < 0) return -1;
-  if (a.fuse_combine) return 1;  // the last split CTA of each unit merged the partials
+  if (a.fuse_combine) {  // the last split CTA of each unit merged the partials
+    if (!hh) return 1;
+    HhPlan hp = *hh;  // the heavy-hitter rows only (no combine blocks)
+    hp.n_units = 0;
+    launch_decode_combine_hh(a, hp, acc_rows, s);
+    return 102;
+  }
   if (hh) {
     launch_decode_combine_hh(a, *hh, acc_rows, s);
     return 102;
