@@ -217,3 +217,18 @@ def test_split_order_configs1_exact_waves():
         n_o.append(o)
         n_q.append(int((8192 - o) * 512 / 144))
     assert A.arkv_split_order_check(c, n_o, n_q, 148) == 592
+
+
+def test_bench_traffic_record_window():
+    """bench.py's roofline traffic comes from the ncu capture of the same kind of step as
+    the timed window: the HH-window capture for the driver's --steps 20 --warmup 5 at
+    configs[1] (all steps before the first decode tailor), the steady capture otherwise."""
+    import argparse
+    import bench
+    key = "auto (split-K chunked pipeline with cost-balanced LPT splits; persistent at >= 32 units per SM)"
+    a = argparse.Namespace(mode="arkv", workload="llama3-8b-32k")
+    hh = bench.traffic_record(a, key, "hh_window")
+    st = bench.traffic_record(a, key, "steady")
+    assert hh and st and hh["dram_bytes_per_launch"] > st["dram_bytes_per_launch"]
+    assert "launch 8" in hh["source"] and "launch 150" in st["source"]
+    assert bench.traffic_record(argparse.Namespace(mode="quant", workload="llama3-8b-32k"), key, "steady") is None
