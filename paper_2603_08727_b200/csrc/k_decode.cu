@@ -296,6 +296,7 @@ static int combine_threads(const Geom& g) { return std::min(1024, std::max(128, 
 // folds rows [chunk * R, chunk * R + R) exactly as decode_hh_acc does.
 // (8 rows per thread run as 256-thread blocks: bounding them at 256 threads leaves the rows'
 // logits and accumulators in registers — at 1024 the 64-register cap spilled them)
+// (3 blocks/SM via launch bounds: spills, step +2 us; not kept)
 template <int G, int kHhRowsPerThread>
 __global__ void __launch_bounds__(kHhRowsPerThread == 8 ? 256 : 1024) decode_combine_hh(DecodeArgs a, const HhPlan hp) {
   griddep_wait();
