@@ -54,6 +54,48 @@ __device__ __forceinline__ void merge_splits(const float* part, int h, int x, in
   }
 }
 
+// Merged (M, L) of every head over the S split partials, computed by one whole warp: lane
+// h + G j takes head h's splits j, j + 32/G, j + 2 (32/G), ... (up to 32/G x kB splits per
+// memory round trip — one round trip for the usual S <= 64 at G = 4, where merge_splits
+// takes ceil(S / 8) dependent ones), then the 32/G lanes of a head fold their (m, l) with
+// a butterfly.  Every lane returns its own head's (M, L).  The sum order differs from
+// merge_splits' (rounding only: both are the flash-decoding reduction of the same terms).
+template <int G>
+__device__ __forceinline__ void merge_ml_warp(const float* part, int lane, int S, int d, float& M, float& L) {
+  constexpr int J = 32 / G;  // lanes per head
+  constexpr int kB = 4;
+  const int h = lane % G, j = lane / G;
+  M = -INFINITY;
+  L = 0.f;
+  for (int s0 = 0; s0 < S; s0 += J * kB) {
+    float m[kB], l[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const int s = s0 + j + k * J;
+      const float* p = part + (s * G + h) * (d + 2);
+      m[k] = s < S ? __ldcg(p) : -INFINITY;
+      l[k] = s < S ? __ldcg(p + 1) : 0.f;
+    }
+    float bm = M;
+#pragma unroll
+    for (int k = 0; k < kB; ++k) bm = fmaxf(bm, m[k]);
+    if (bm == -INFINITY) continue;
+    if (M != -INFINITY) L *= exp2f(M - bm);
+    M = bm;
+#pragma unroll
+    for (int k = 0; k < kB; ++k)
+      if (m[k] != -INFINITY) L += l[k] * exp2f(m[k] - M);
+  }
+#pragma unroll
+  for (int off = G; off < 32; off <<= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, M, off), l2 = __shfl_xor_sync(0xffffffffu, L, off);
+    const float mn = fmaxf(M, m2);
+    if (mn != -INFINITY)
+      L = (M != -INFINITY ? L * exp2f(M - mn) : 0.f) + (m2 != -INFINITY ? l2 * exp2f(m2 - mn) : 0.f);
+    M = mn;
+  }
+}
+
 template <int G>
 __device__ __forceinline__ void combine_unit(const DecodeArgs& a, int u, int b, int li, int kvh, const UnitDesc& dsc,
                                              float* /*sM*/, float* /*sIL*/) {
@@ -62,21 +104,73 @@ __device__ __forceinline__ void combine_unit(const DecodeArgs& a, int u, int b, 
   const int S = a.nsplit ? a.nsplit[u] : a.n_splits;
   const float* part = a.partials + (int64_t)u * a.max_splits * G * (d + 2);
   const int64_t obase = ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * G) * d;
-  // one thread per (head, dim); each merges its head's split statistics itself (redundant
-  // across the head's d threads, but no shared-memory round and no __syncthreads)
-  for (int idx = threadIdx.x; idx < G * d; idx += blockDim.x) {
-    const int h = idx / d, x = idx % d;
-    float M, L, O;
-    merge_splits<G, true>(part, h, x, S, d, M, L, O);
-    const float IL = 1.0f / L;
-    O *= IL;
-    if (a.out_fp32)
-      ((float*)a.out)[obase + idx] = O;
-    else
-      ((uint16_t*)a.out)[obase + idx] = f_to_bf16_rne(O);
-    if (x == 0) {
-      a.mstat[((int64_t)u * G + h) * 2 + 0] = M;
-      a.mstat[((int64_t)u * G + h) * 2 + 1] = IL;
+#ifndef ARKV_COMBINE_WARP_MERGE
+#define ARKV_COMBINE_WARP_MERGE 1
+#endif
+  if constexpr (ARKV_COMBINE_WARP_MERGE != 0) {
+    // every warp merges all heads' (M, L) with all 32 lanes (merge_ml_warp: one round trip),
+    // then each thread (head, dim) sums its S output partials at the known M: the loads of
+    // a batch of kB splits are independent (no running rescale between batches)
+    const int lane = threadIdx.x & 31;
+    float Mw, Lw;
+    merge_ml_warp<G>(part, lane, S, d, Mw, Lw);
+    float wM[G], wL[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      wM[h] = __shfl_sync(0xffffffffu, Mw, h);
+      wL[h] = __shfl_sync(0xffffffffu, Lw, h);
+    }
+    for (int idx = threadIdx.x; idx < G * d; idx += blockDim.x) {
+      const int h = idx / d, x = idx % d;
+      float M = wM[0], L = wL[0];
+#pragma unroll
+      for (int k = 1; k < G; ++k)
+        if (h == k) {
+          M = wM[k];
+          L = wL[k];
+        }
+      constexpr int kB = 8;  // 16 spills under the 1024-thread bound (64 registers)
+      float O = 0.f;
+      for (int s0 = 0; s0 < S; s0 += kB) {
+        float m[kB], o[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          const float* p = part + ((s0 + j) * G + h) * (d + 2);
+          m[j] = s0 + j < S ? __ldcg(p) : -INFINITY;
+          o[j] = s0 + j < S ? __ldcg(p + 2 + x) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j)
+          if (m[j] != -INFINITY) O += o[j] * exp2f(m[j] - M);
+      }
+      const float IL = 1.0f / L;
+      O *= IL;
+      if (a.out_fp32)
+        ((float*)a.out)[obase + idx] = O;
+      else
+        ((uint16_t*)a.out)[obase + idx] = f_to_bf16_rne(O);
+      if (x == 0) {
+        a.mstat[((int64_t)u * G + h) * 2 + 0] = M;
+        a.mstat[((int64_t)u * G + h) * 2 + 1] = IL;
+      }
+    }
+  } else {
+    // one thread per (head, dim); each merges its head's split statistics itself (redundant
+    // across the head's d threads, but no shared-memory round and no __syncthreads)
+    for (int idx = threadIdx.x; idx < G * d; idx += blockDim.x) {
+      const int h = idx / d, x = idx % d;
+      float M, L, O;
+      merge_splits<G, true>(part, h, x, S, d, M, L, O);
+      const float IL = 1.0f / L;
+      O *= IL;
+      if (a.out_fp32)
+        ((float*)a.out)[obase + idx] = O;
+      else
+        ((uint16_t*)a.out)[obase + idx] = f_to_bf16_rne(O);
+      if (x == 0) {
+        a.mstat[((int64_t)u * G + h) * 2 + 0] = M;
+        a.mstat[((int64_t)u * G + h) * 2 + 1] = IL;
+      }
     }
   }
   if (threadIdx.x == 0) {

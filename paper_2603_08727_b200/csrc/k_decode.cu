@@ -287,13 +287,20 @@ __global__ void __launch_bounds__(256) decode_hh_acc(DecodeArgs a) {
   }
 }
 
+#ifndef ARKV_HH_LANE_MERGE
+#define ARKV_HH_LANE_MERGE 1
+#endif
+constexpr bool kHhLaneMerge = ARKV_HH_LANE_MERGE != 0;
+
 // one combine thread per (head, dim) up to 1024 (measured: latency-bound otherwise)
 static int combine_threads(const Geom& g) { return std::min(1024, std::max(128, (g.G * g.d + 31) / 32 * 32)); }
 
 // Split combine with the step's HH accumulation in the same grid (saves the separate
 // decode_hh_acc launch and its drain).  Combine blocks as decode_combine; an HH block
-// recomputes its unit's merged (M, 1/L) with the combine's own code (bit-identical), then
-// folds rows [chunk * R, chunk * R + R) exactly as decode_hh_acc does.
+// recomputes its unit's merged (M, 1/L) with the combine's own code (merge_ml_warp, all 32
+// lanes of each warp: bit-identical to the M, L the combine normalises the output with;
+// ARKV_HH_LANE_MERGE=0 with ARKV_COMBINE_WARP_MERGE=0 is round 2's lane-per-head merge) —
+// then folds rows [chunk * R, chunk * R + R) exactly as decode_hh_acc does.
 // (8 rows per thread run as 256-thread blocks: bounding them at 256 threads leaves the rows'
 // logits and accumulators in registers — at 1024 the 64-register cap spilled them)
 // (3 blocks/SM via launch bounds: spills, step +2 us; not kept)
@@ -365,7 +372,20 @@ __global__ void __launch_bounds__(kHhRowsPerThread == 8 ? 256 : 1024) decode_com
   // with the combine's code, bit for bit, and broadcasts it): no block barrier between the
   // rows' loads and their use (a __syncthreads here was the kernel's top stall)
   float sM[G], sIL[G];
-  {
+  if constexpr (kHhLaneMerge) {
+    // the whole warp merges (one memory round trip instead of ceil(S / 8) dependent ones);
+    // lane h holds head h's result
+    const int lane = threadIdx.x & 31;
+    const float* part = a.partials + (int64_t)u * a.max_splits * G * (g.d + 2);
+    float M, L;
+    merge_ml_warp<G>(part, lane, S_hh, g.d, M, L);
+    const float ilh = 1.0f / L;
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      sM[h] = __shfl_sync(0xffffffffu, M, h);
+      sIL[h] = __shfl_sync(0xffffffffu, ilh, h);
+    }
+  } else {
     const int lane = threadIdx.x & 31;
     float mh = 0.f, ilh = 0.f;
     if (lane < G) {
