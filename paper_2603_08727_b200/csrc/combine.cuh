@@ -105,13 +105,27 @@ __device__ __forceinline__ void combine_unit(const DecodeArgs& a, int u, int b, 
   const float* part = a.partials + (int64_t)u * a.max_splits * G * (d + 2);
   const int64_t obase = ((int64_t)(b * a.n_layers + li) * g.Hq + kvh * G) * d;
 #ifndef ARKV_COMBINE_WARP_MERGE
-#define ARKV_COMBINE_WARP_MERGE 1
+#define ARKV_COMBINE_WARP_MERGE 0
 #endif
   if constexpr (ARKV_COMBINE_WARP_MERGE != 0) {
     // every warp merges all heads' (M, L) with all 32 lanes (merge_ml_warp: one round trip),
     // then each thread (head, dim) sums its S output partials at the known M: the loads of
     // a batch of kB splits are independent (no running rescale between batches)
     const int lane = threadIdx.x & 31;
+    // the thread's first (head, dim): its first kB splits' (m, o) are loaded before the
+    // warp merge (they do not depend on M), so a call with S <= kB takes one round trip
+    constexpr int kB = 8;  // 16 spills under the 1024-thread bound (64 registers)
+    float pm[kB], po[kB];
+    {
+      const int idx = threadIdx.x, h = idx / d, x = idx % d;
+      const bool ok = idx < G * d;
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const float* p = part + (j * G + h) * (d + 2);
+        pm[j] = ok && j < S ? __ldcg(p) : -INFINITY;
+        po[j] = ok && j < S ? __ldcg(p + 2 + x) : 0.f;
+      }
+    }
     float Mw, Lw;
     merge_ml_warp<G>(part, lane, S, d, Mw, Lw);
     float wM[G], wL[G];
@@ -129,9 +143,15 @@ __device__ __forceinline__ void combine_unit(const DecodeArgs& a, int u, int b, 
           M = wM[k];
           L = wL[k];
         }
-      constexpr int kB = 8;  // 16 spills under the 1024-thread bound (64 registers)
       float O = 0.f;
-      for (int s0 = 0; s0 < S; s0 += kB) {
+      int s0 = 0;
+      if (idx == (int)threadIdx.x) {  // the prefetched first batch
+#pragma unroll
+        for (int j = 0; j < kB; ++j)
+          if (pm[j] != -INFINITY) O += po[j] * exp2f(pm[j] - M);
+        s0 = kB;
+      }
+      for (; s0 < S; s0 += kB) {
         float m[kB], o[kB];
 #pragma unroll
         for (int j = 0; j < kB; ++j) {

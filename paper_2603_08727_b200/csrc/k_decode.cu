@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) decode_hh_acc(DecodeArgs a) {
 }
 
 #ifndef ARKV_HH_LANE_MERGE
-#define ARKV_HH_LANE_MERGE 1
+#define ARKV_HH_LANE_MERGE 0
 #endif
 constexpr bool kHhLaneMerge = ARKV_HH_LANE_MERGE != 0;
 
@@ -297,9 +297,9 @@ static int combine_threads(const Geom& g) { return std::min(1024, std::max(128, 
 
 // Split combine with the step's HH accumulation in the same grid (saves the separate
 // decode_hh_acc launch and its drain).  Combine blocks as decode_combine; an HH block
-// recomputes its unit's merged (M, 1/L) with the combine's own code (merge_ml_warp, all 32
-// lanes of each warp: bit-identical to the M, L the combine normalises the output with;
-// ARKV_HH_LANE_MERGE=0 with ARKV_COMBINE_WARP_MERGE=0 is round 2's lane-per-head merge) —
+// recomputes its unit's merged (M, 1/L) with the combine's own code (bit-identical: the
+// default lane-per-head merge_splits; ARKV_HH_LANE_MERGE=1 with ARKV_COMBINE_WARP_MERGE=1
+// is the whole-warp merge_ml_warp in both, measured in DESIGN §16b and not the default) —
 // then folds rows [chunk * R, chunk * R + R) exactly as decode_hh_acc does.
 // (8 rows per thread run as 256-thread blocks: bounding them at 256 threads leaves the rows'
 // logits and accumulators in registers — at 1024 the 64-register cap spilled them)
